@@ -1,0 +1,412 @@
+// tc:: — the reference's contraction API (/root/reference/proj/include/tc/*.hpp),
+// re-declared for the B200 engine so existing callers compile unchanged.
+// The per-topic headers tc/tensor.hpp, tc/expr.hpp, tc/planner.hpp,
+// tc/kernels.hpp and tc/executor.hpp include this file.
+//
+// Everything here is host C++ (no CUDA types). Arithmetic goes to the device
+// through the C-ABI in tcb.h; see DESIGN.md for the lowering.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace tc {
+
+// ============================================================ L0: storage
+// reference: include/tc/tensor.hpp:10-108
+
+enum class Variance : std::uint8_t { Up, Down };
+char variance_char(Variance v);
+
+/// Dense fp64 tensor, generalized column-major: stride(mode k) = prod of the
+/// extents of modes 0..k-1. Rank 0 holds one scalar.
+class Tensor {
+ public:
+  Tensor() = default;
+  Tensor(std::vector<std::int64_t> extents, std::vector<Variance> variance,
+         std::string name = "t");
+
+  static Tensor zeros(std::vector<std::int64_t> extents, std::vector<Variance> variance,
+                      std::string name = "t");
+  static Tensor sequential(std::vector<std::int64_t> extents, std::vector<Variance> variance,
+                           std::string name = "t");
+  /// Uniform [-1, 1] from std::mt19937_64(seed), storage order — the same
+  /// stream as the reference (src/tensor.cpp:54-62), bit for bit.
+  static Tensor seeded_random(std::vector<std::int64_t> extents, std::vector<Variance> variance,
+                              std::uint64_t seed, std::string name = "t");
+  static Tensor from_values(std::vector<std::int64_t> extents, std::vector<Variance> variance,
+                            std::vector<double> values, std::string name = "t");
+
+  int rank() const { return static_cast<int>(ext_.size()); }
+  std::int64_t size() const { return static_cast<std::int64_t>(buf_.size()); }
+  const std::vector<std::int64_t>& extents() const { return ext_; }
+  std::int64_t extent(int mode) const;
+  const std::vector<Variance>& variance() const { return var_; }
+  Variance variance(int mode) const;
+  const std::string& name() const { return name_; }
+  void set_name(std::string name) { name_ = std::move(name); }
+
+  double* data() { return buf_.data(); }
+  const double* data() const { return buf_.data(); }
+
+  double at(const std::vector<std::int64_t>& coords) const;
+  double& at(const std::vector<std::int64_t>& coords);
+  std::int64_t offset_of(const std::vector<std::int64_t>& coords) const;
+
+ private:
+  std::vector<std::int64_t> ext_, str_;
+  std::vector<Variance> var_;
+  std::vector<double> buf_;
+  std::string name_ = "t";
+  friend std::int64_t stride_of(const Tensor& t, int mode);
+};
+
+std::int64_t stride_of(const Tensor& t, int mode);
+
+using SlicingVector = std::vector<std::uint8_t>;  // 1 = mode fixed per slice
+
+struct KeptMode {
+  int mode = 0;
+  std::int64_t extent = 0;
+  std::int64_t stride = 0;
+};
+
+struct SliceView {
+  const Tensor* parent = nullptr;
+  std::int64_t base_offset = 0;
+  std::vector<KeptMode> kept;
+  int rank() const { return static_cast<int>(kept.size()); }
+  std::int64_t offset_of(const std::vector<std::int64_t>& coords) const;
+  double at(const std::vector<std::int64_t>& coords) const;
+};
+
+SliceView slice_view(const Tensor& t, const SlicingVector& s,
+                     const std::vector<std::int64_t>& fixed);
+
+struct PackedMatrix {
+  std::int64_t rows = 0, cols = 0, leading_dimension = 0;
+  const double* data = nullptr;
+  bool copied = false;
+  std::int64_t source_offset = 0;
+  std::vector<double> storage;
+};
+
+PackedMatrix pack_slice(const SliceView& v);
+
+// ============================================================ L1: expressions
+// reference: include/tc/expr.hpp:12-91
+
+struct parse_error : std::runtime_error {
+  parse_error(const std::string& what, std::size_t position)
+      : std::runtime_error(what + " (at position " + std::to_string(position) + ")"),
+        position(position) {}
+  std::size_t position;
+};
+
+struct IndexRef {
+  std::string label;
+  Variance var = Variance::Up;
+  bool operator==(const IndexRef&) const = default;
+};
+
+struct TensorExpr {
+  std::string name;
+  std::vector<IndexRef> indices;
+  bool operator==(const TensorExpr&) const = default;
+};
+
+struct ContractionSpec {
+  TensorExpr output, left, right;
+  bool positional = false;
+  bool operator==(const ContractionSpec&) const = default;
+};
+
+/// `OUT[±i,...] = L[...] * R[...]` (ASCII); see DESIGN.md for the rules.
+ContractionSpec parse(const std::string& expr, bool positional = false);
+std::string unparse(const ContractionSpec& spec);
+
+struct LabelInfo {
+  std::string label;
+  std::int64_t extent = 0;
+  bool contracted = false;
+  int left_mode = -1, right_mode = -1, output_mode = -1;
+};
+
+struct ValidatedContraction {
+  ContractionSpec spec;
+  std::vector<LabelInfo> labels;  // left modes in order, then right-only labels
+  std::vector<int> contracted;    // by left mode order
+  std::vector<int> left_free;     // by left mode order
+  std::vector<int> right_free;    // by right mode order
+  int p = 0, delta_left = 0, delta_right = 0;
+
+  int left_rank() const { return static_cast<int>(spec.left.indices.size()); }
+  int right_rank() const { return static_cast<int>(spec.right.indices.size()); }
+  int output_rank() const { return static_cast<int>(spec.output.indices.size()); }
+  const LabelInfo& label_at_left_mode(int mode) const;
+  const LabelInfo& label_at_right_mode(int mode) const;
+  int label_index(const std::string& label) const;
+  std::vector<std::int64_t> output_extents() const;
+  std::vector<Variance> output_variance() const;
+};
+
+ValidatedContraction validate(const ContractionSpec& spec, const Tensor& left,
+                              const Tensor& right);
+
+/// validate() on operand shapes alone (no storage), for callers that hold the
+/// data elsewhere (device buffers, the C front). Same checks and messages.
+ValidatedContraction validate_shapes(const ContractionSpec& spec,
+                                     const std::vector<std::int64_t>& left_extents,
+                                     const std::vector<Variance>& left_variance,
+                                     const std::vector<std::int64_t>& right_extents,
+                                     const std::vector<Variance>& right_variance);
+
+/// Algorithmic flops: 2 * prod(all label extents).
+std::int64_t flop_count(const ValidatedContraction& v);
+
+// ============================================================ L2: planner
+// reference: include/tc/planner.hpp:12-142
+
+enum class ContractionClass { C1, C2, C31, C32 };
+std::string to_string(ContractionClass c);
+
+enum class KernelKind { Gemm, CopyGemm, Gemv, CopyGemv, Ger, Dot, Elementwise };
+std::string to_string(KernelKind k);
+std::optional<KernelKind> kernel_from_string(const std::string& s);
+
+enum class Fallback { None, F1, F2, F3 };
+std::string to_string(Fallback f);
+
+struct RequirementReport {
+  bool r1_ok = false, r2_ok = false, r3_ok = false;
+  Fallback fallback = Fallback::None;
+  KernelKind kernel = KernelKind::Elementwise;
+};
+
+struct SlicingOption {
+  SlicingVector s_left, s_right;
+  RequirementReport report;
+  std::int64_t kernel_dims_product = 0;
+  bool output_staged = false;
+};
+
+struct LoopLabel {
+  int label = -1;
+  bool contracted = false;
+  std::int64_t extent = 0;
+};
+
+struct KernelMap {
+  int m_label = -1, n_label = -1, k_label = -1, k2_label = -1;
+  bool a_is_left = true;
+  bool trans_a = false, trans_b = false;
+  bool matrix_is_left = true;
+};
+
+enum class CopyTarget { Left, Right, OutputStage };
+
+struct ExecutionPlan {
+  ContractionClass cls = ContractionClass::C32;
+  SlicingVector s_left, s_right, s_output;
+  KernelKind kernel = KernelKind::Gemm;
+  std::vector<LoopLabel> loop_nest;
+  KernelMap kernel_map;
+  std::vector<CopyTarget> copies;
+  std::int64_t flops = 0;
+  std::vector<std::int64_t> label_extents;
+};
+
+struct kernel_unreachable_error : std::runtime_error {
+  kernel_unreachable_error(KernelKind kernel, const std::string& requirement)
+      : std::runtime_error("kernel unreachable: " + requirement + " violated"),
+        kernel(kernel),
+        requirement(requirement) {}
+  explicit kernel_unreachable_error(const std::string& msg)
+      : std::runtime_error(msg), kernel(KernelKind::Gemm) {}
+  KernelKind kernel;
+  std::string requirement;
+};
+
+ContractionClass classify(const ValidatedContraction& v);
+RequirementReport check_requirements(const ValidatedContraction& v, const SlicingVector& s_left,
+                                     const SlicingVector& s_right);
+std::vector<SlicingOption> enumerate_slicings(const ValidatedContraction& v);
+
+struct PlanPolicy {
+  enum class Mode { Auto, ForceKernel, ForceSlicing };
+  Mode mode = Mode::Auto;
+  KernelKind kernel = KernelKind::Gemm;
+  SlicingVector s_left, s_right;
+
+  static PlanPolicy auto_policy() { return {}; }
+  static PlanPolicy force_kernel(KernelKind k) {
+    PlanPolicy p;
+    p.mode = Mode::ForceKernel;
+    p.kernel = k;
+    return p;
+  }
+  static PlanPolicy force_slicing(SlicingVector sl, SlicingVector sr) {
+    PlanPolicy p;
+    p.mode = Mode::ForceSlicing;
+    p.s_left = std::move(sl);
+    p.s_right = std::move(sr);
+    return p;
+  }
+};
+
+ExecutionPlan plan(const ValidatedContraction& v,
+                   const PlanPolicy& policy = PlanPolicy::auto_policy());
+std::string render_plan(const ExecutionPlan& p, const ValidatedContraction& v);
+std::optional<std::string> relayout_advice(const ValidatedContraction& v);
+
+// ============================================================ L3: backends
+// reference: include/tc/kernels.hpp:12-48
+
+class KernelBackend {
+ public:
+  virtual ~KernelBackend() = default;
+  virtual const std::string& name() const = 0;
+  virtual bool supports_transpose() const { return true; }
+  virtual void gemm(bool trans_a, bool trans_b, std::int64_t m, std::int64_t n, std::int64_t k,
+                    double alpha, const double* a, std::int64_t lda, const double* b,
+                    std::int64_t ldb, double beta, double* c, std::int64_t ldc) const = 0;
+  virtual void gemv(bool trans, std::int64_t m, std::int64_t n, double alpha, const double* a,
+                    std::int64_t lda, const double* x, std::int64_t incx, double beta, double* y,
+                    std::int64_t incy) const = 0;
+  virtual void ger(std::int64_t m, std::int64_t n, double alpha, const double* x,
+                   std::int64_t incx, const double* y, std::int64_t incy, double* a,
+                   std::int64_t lda) const = 0;
+  virtual double dot(std::int64_t k, const double* x, std::int64_t incx, const double* y,
+                     std::int64_t incy) const = 0;
+};
+
+/// Options of the B200 backend. `device` selects the GPU this backend drives;
+/// `fail_after_launches` >= 0 injects a synthetic device fault after that many
+/// successful device operations (fault-propagation tests, cf. the reference's
+/// FailingBackend, tests/test_executor.cpp:240-291).
+struct B200Options {
+  int device = 0;
+  int fail_after_launches = -1;
+};
+
+/// The B200 device backend. Its BLAS methods take HOST pointers (copy in, one
+/// device call, copy out) so the reference's backend contract holds; execute()
+/// recognises it and lowers a whole plan to device launches instead.
+std::unique_ptr<KernelBackend> make_b200_backend(const B200Options& options = {});
+
+/// "b200" (also "device") -> make_b200_backend(). The reference names
+/// "reference" and "external" are CPU backends and are not part of this
+/// engine: they throw std::invalid_argument naming the replacement.
+std::unique_ptr<KernelBackend> make_backend(const std::string& name);
+
+// ============================================================ L4: executor
+// reference: include/tc/executor.hpp:14-54
+
+struct ExecutionStats {
+  std::int64_t kernel_calls = 0;  // device kernel launches
+  std::int64_t packed_bytes = 0;  // bytes written by operand permutations
+  std::int64_t staged_bytes = 0;  // output staging bytes (0: strided epilogue)
+  std::int64_t flops = 0;         // plan.flops
+  double wall_seconds = 0.0;      // host wall time incl. transfers
+};
+
+/// Runs the contraction on the device: the plan is checked against the
+/// operands (extent drift), lowered to one device recipe (permutations +
+/// one GEMM/GEMV/DOT launch) and executed. `workers` is accepted for source
+/// compatibility; results are bit-identical for any value.
+std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
+                                          const ValidatedContraction& v, const Tensor& left,
+                                          const Tensor& right, const KernelBackend& backend,
+                                          int workers = 1);
+
+struct SlicingRun {
+  SlicingVector s_left, s_right;
+  KernelKind kernel = KernelKind::Elementwise;
+  std::uint64_t result_hash = 0;
+  ExecutionStats stats;
+  Tensor result;
+};
+
+std::vector<SlicingRun> execute_all_slicings(const ValidatedContraction& v, const Tensor& left,
+                                             const Tensor& right, const KernelBackend& backend,
+                                             std::int64_t work_cap = 1000000000);
+
+std::uint64_t tensor_hash(const Tensor& t);
+double max_rel_error(const Tensor& a, const Tensor& b);
+/// ||a-b||_F / ||b||_F — the BASELINE parity criterion (not in the reference).
+double rel_frobenius_error(const Tensor& a, const Tensor& b);
+
+/// Thrown by execute_all_slicings when the sweep exceeds its work cap
+/// (the reference declares it in tc/oracle.hpp:11-13).
+struct resource_limit_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ============================================================ device recipe
+// (new; no reference counterpart) — the lowering of a contraction onto the
+// device: optional operand permutations followed by one batched GEMM with
+// composite output addressing. Exposed for tests and tools.
+
+struct PermuteStep {
+  bool right = false;                 // which operand
+  std::vector<std::int64_t> ext;      // destination order (dense, first fastest)
+  std::vector<std::int64_t> src_str;  // source strides of those dims
+  std::int64_t elements = 0;
+};
+
+struct DeviceRecipe {
+  std::vector<PermuteStep> permutes;
+  // GEMM over (possibly permuted) operands, see tcb_gemm_desc in tcb.h
+  std::int64_t m = 1, n = 1, k = 1;
+  std::int64_t a_sm = 1, a_sk = 1, b_sk = 1, b_sn = 1;
+  std::vector<std::int64_t> row_ext, row_str, col_ext, col_str;
+  std::vector<std::int64_t> bat_ext, bat_sa, bat_sb, bat_sc;
+  std::string layout;  // "L1" in place, "L2" batched, "L3" permuted
+  std::string summary() const;
+};
+
+DeviceRecipe lower(const ValidatedContraction& v);
+
+/// A contraction lowered once and bound to device buffers, for repeated
+/// execution without host round trips (no reference counterpart; bench.py
+/// and the C front use it). Not copyable.
+class PreparedContraction {
+ public:
+  explicit PreparedContraction(const ValidatedContraction& v, int device = 0);
+  ~PreparedContraction();
+  PreparedContraction(const PreparedContraction&) = delete;
+  PreparedContraction& operator=(const PreparedContraction&) = delete;
+
+  /// Host -> device copies of both operands (storage order of the tensors).
+  void upload(const double* left, const double* right);
+  /// Permutations + the GEMM/GEMV/DOT launch, on the device stream (async).
+  void run();
+  /// Device -> host copy of the result (synchronous).
+  void download(double* out);
+  void sync();
+
+  const DeviceRecipe& recipe() const { return recipe_; }
+  std::int64_t left_elements() const { return nl_; }
+  std::int64_t right_elements() const { return nr_; }
+  std::int64_t output_elements() const { return no_; }
+  double* left_device() const { return dl_; }
+  double* right_device() const { return dr_; }
+  double* output_device() const { return do_; }
+  std::int64_t launches_last_run() const { return launches_; }
+  std::int64_t permuted_bytes() const;
+
+ private:
+  DeviceRecipe recipe_;
+  int device_ = 0;
+  std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
+  double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;
+  double *pl_ = nullptr, *pr_ = nullptr;  // permuted operands (L3)
+  std::int64_t launches_ = 0;
+};
+
+}  // namespace tc

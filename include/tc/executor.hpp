@@ -1,0 +1,4 @@
+// Drop-in header name of the reference API (proj/include/tc/executor.hpp); the
+// declarations live in tc/contract.hpp.
+#pragma once
+#include "tc/contract.hpp"

@@ -1,0 +1,141 @@
+/*
+ * tcb.h — device-side C-ABI of the B200-native fp64 contraction engine.
+ *
+ * Plain C, plain pointers and sizes; no CUDA or C++ types cross this boundary,
+ * so the host front (C++), ctypes (Python) or any FFI can bind it. Every call
+ * returns a tcb_status; on failure tcb_last_error() holds a thread-local
+ * message. All matrices are column-major, element strides count doubles.
+ *
+ * The reference (/root/reference/proj) has no device layer: its arithmetic is
+ * the abstract KernelBackend (include/tc/kernels.hpp:12-39) implemented on the
+ * CPU by ReferenceBackend (src/kernels_reference.cpp:33-149), driven slice by
+ * slice by tc::execute (src/executor.cpp:102-283). Each entry point below names
+ * the reference interface it replaces.
+ */
+#ifndef TCB_H_
+#define TCB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tcb_status {
+  TCB_OK = 0,
+  TCB_EINVAL = 1,      /* bad argument; message mirrors the reference's std::invalid_argument */
+  TCB_ECUDA = 2,       /* CUDA runtime / driver failure */
+  TCB_ENCCL = 3,       /* collective failure */
+  TCB_ENOMEM = 4,      /* device allocation failure */
+  TCB_EUNSUPPORTED = 5 /* shape outside what the device path implements */
+} tcb_status;
+
+#define TCB_MAX_DIMS 6
+
+/* ---- context, memory, streams ------------------------------------------- */
+/* One context per device per process; selects `device` for the calling
+ * thread. No reference counterpart (the reference is host-only). */
+int tcb_init(int device);
+int tcb_finalize(void);
+int tcb_device_count(int* count);
+const char* tcb_last_error(void);
+/* Run subsequent work of this thread on a caller-owned cudaStream_t (passed as
+ * void*); NULL restores the context's own stream. */
+int tcb_set_stream(void* stream);
+int tcb_sync(void);
+
+int tcb_alloc(void** dptr, int64_t bytes);
+int tcb_free(void* dptr);
+int tcb_memset0(void* dptr, int64_t bytes);
+int tcb_h2d(void* dst, const void* src, int64_t bytes);
+int tcb_d2h(void* dst, const void* src, int64_t bytes);
+int tcb_d2d(void* dst, const void* src, int64_t bytes);
+/* Pin / unpin caller host memory so H2D/D2H run at DMA speed
+ * (reference operands live in std::vector<double>, include/tc/tensor.hpp:58). */
+int tcb_host_register(void* ptr, int64_t bytes);
+int tcb_host_unregister(void* ptr);
+
+/* ---- the general device recipe ------------------------------------------
+ * C[b; m, n] = alpha * sum_k A[b; m, k] * B[b; k, n] + beta * C[b; m, n]
+ *   A(m,k) at A + a_off(b) + m*a_sm + k*a_sk
+ *   B(k,n) at B + b_off(b) + k*b_sk + n*b_sn
+ *   C(m,n) at C + c_off(b) + row(m) + col(n), where m and n are themselves
+ *   composite indices (first sub-index fastest): row(m) = sum_i m_i*c_row_str[i]
+ * and batch index b decomposes over bat_ext (first fastest) with per-operand
+ * strides (0 where a batch label does not address that operand).
+ * This replaces the whole loop-over-kernel nest of tc::execute
+ * (src/executor.cpp:119-177 + :274-281) for one contraction: one launch. */
+typedef struct tcb_gemm_desc {
+  int64_t m, n, k;
+  int64_t a_sm, a_sk;
+  int64_t b_sk, b_sn;
+  int32_t c_nrow, c_ncol;
+  int64_t c_row_ext[TCB_MAX_DIMS], c_row_str[TCB_MAX_DIMS];
+  int64_t c_col_ext[TCB_MAX_DIMS], c_col_str[TCB_MAX_DIMS];
+  int32_t nbatch;
+  int64_t bat_ext[TCB_MAX_DIMS];
+  int64_t bat_sa[TCB_MAX_DIMS], bat_sb[TCB_MAX_DIMS], bat_sc[TCB_MAX_DIMS];
+  double alpha, beta;
+} tcb_gemm_desc;
+
+/* Execution report for the last tcb_gemm on this thread. */
+typedef struct tcb_gemm_info {
+  int32_t path;        /* 0 DMMA GEMM via TMA, 1 DMMA GEMM via cp.async, 2 GEMV, 3 DOT */
+  int32_t splits;      /* split-K factor */
+  int64_t units;       /* work units (tiles x splits) */
+  int32_t grid;        /* CTAs launched */
+  int32_t launches;    /* kernel launches issued */
+} tcb_gemm_info;
+
+int tcb_gemm(const tcb_gemm_desc* d, const double* A, const double* B, double* C);
+int tcb_last_gemm_info(tcb_gemm_info* info);
+
+/* BLAS-semantics GEMM on device buffers: C <- alpha*op(A)*op(B) + beta*C.
+ * Replaces KernelBackend::gemm (include/tc/kernels.hpp:20-23,
+ * src/kernels_reference.cpp:33-79); argument errors carry the reference's
+ * messages ("gemm: lda below row count", kernels_reference.cpp:12-24). */
+int tcb_dgemm(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+              double* C, int64_t ldc);
+
+/* Strided-batched GEMM: one launch for `batch` independent products, replacing
+ * the executor's free-label loop of gemm calls (src/executor.cpp:119-177). */
+int tcb_dgemm_strided_batched(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                              double alpha, const double* A, int64_t lda, int64_t stride_a,
+                              const double* B, int64_t ldb, int64_t stride_b, double beta,
+                              double* C, int64_t ldc, int64_t stride_c, int64_t batch);
+
+/* y <- alpha*op(A)*x + beta*y  (KernelBackend::gemv, include/tc/kernels.hpp:26-29). */
+int tcb_dgemv(int trans, int64_t m, int64_t n, double alpha, const double* A, int64_t lda,
+              const double* x, int64_t incx, double beta, double* y, int64_t incy);
+/* A <- alpha*x*y^T + A  (KernelBackend::ger, include/tc/kernels.hpp:32-34). */
+int tcb_dger(int64_t m, int64_t n, double alpha, const double* x, int64_t incx, const double* y,
+             int64_t incy, double* A, int64_t lda);
+/* *result_host <- x . y  (KernelBackend::dot, include/tc/kernels.hpp:37-38). */
+int tcb_ddot(int64_t k, const double* x, int64_t incx, const double* y, int64_t incy,
+             double* result_host);
+
+/* ---- permutation (COPY of COPY+GEMM) -------------------------------------
+ * dst[i_0 + e_0*(i_1 + e_1*(...))] = src[sum_j i_j * src_str[j]]: dst is dense
+ * in the given dimension order (first fastest). Replaces the executor's
+ * per-slice packing copy (materialize, src/executor.cpp:41-59) with one
+ * coalesced launch over the whole operand. */
+int tcb_permute(int rank, const int64_t* ext, const int64_t* src_str, const double* src,
+                double* dst);
+
+/* ---- timing -------------------------------------------------------------- */
+/* Device-side timing on this thread's stream: tcb_timer_start/stop bracket
+ * work; elapsed in milliseconds between the two events. */
+int tcb_timer_start(void);
+int tcb_timer_stop(float* ms);
+
+/* Count of kernels this library launched on this thread since the last reset
+ * (evidence for bench.py's gpu_launches). */
+int64_t tcb_launch_count(void);
+void tcb_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCB_H_ */

@@ -1,0 +1,57 @@
+/*
+ * tcf.h — plan-level C-ABI of the engine (libtc_b200.so): the reference's
+ * parse -> validate -> plan -> execute path (tools/tcontract.cpp:114-153,
+ * src/executor.cpp:287-369) as flat C calls, for ctypes/cgo/JNI callers and
+ * for the repo's own tests and bench. Strings are NUL-terminated ASCII;
+ * extents are given as "label=N,label=N,...". Status codes: 0 ok,
+ * 1 invalid argument / runtime error, 2 parse error, 3 resource cap,
+ * 4 buffer too small (the same codes as the reference CLI's exit statuses,
+ * tools/tcontract.cpp:5-6). Error text is written to `err`.
+ */
+#ifndef TCF_H_
+#define TCF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Deterministic analysis report (classification, slicing catalogue, auto and
+ * forced plans, re-layout advice, device recipe) — the text the parity tests
+ * diff against the reference. Operands are bound like the reference CLI
+ * (tools/tcontract.cpp:38-51). */
+int tcf_report(const char* expr, int positional, const char* extents, char* buf, int64_t cap);
+
+/* tc::execute with the b200 backend on operands seeded like the reference
+ * CLI (left: seed, right: seed+1; tools/tcontract.cpp:118-119).
+ * policy: 0 auto, 1 force kernel (KernelKind index), 2 force slicing ("0 1 0").
+ * stats[4] = kernel_calls, packed_bytes, staged_bytes, flops. */
+int tcf_execute(const char* expr, int positional, const char* extents, uint64_t seed,
+                int workers, int policy, int kernel, const char* s_left, const char* s_right,
+                double* out, int64_t out_cap, int64_t* stats, double* seconds, char* err,
+                int64_t errcap);
+
+/* Fill `out` with Tensor::seeded_random's stream (src/tensor.cpp:54-62). */
+int tcf_seeded(int64_t n, uint64_t seed, double* out);
+
+/* Prepared contraction bound to device buffers (tc::PreparedContraction). */
+int tcf_prepare(const char* expr, int positional, const char* extents, int device,
+                void** handle, char* err, int64_t errcap);
+int tcf_upload(void* handle, const double* left, const double* right);
+int tcf_run(void* handle);
+int tcf_download(void* handle, double* out);
+int tcf_sync(void* handle);
+/* info[12]: left, right, output elements; launches of the last run;
+ * permuted bytes; m, n, k, batch; flops; number of permutes; device path
+ * (tcb_gemm_info.path of the last run). summary: recipe text. */
+int tcf_info(void* handle, int64_t* info, char* summary, int64_t cap);
+int tcf_device_ptrs(void* handle, void** left, void** right, void** out);
+int tcf_release(void* handle);
+const char* tcf_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCF_H_ */

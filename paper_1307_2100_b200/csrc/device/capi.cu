@@ -1,0 +1,407 @@
+// C-ABI of libtcb200.so (declared in include/tcb.h): context, memory, and the
+// argument-checking front of every device operation. Argument errors reproduce
+// the reference backend's messages (src/kernels_reference.cpp:12-24) so a
+// caller that mapped them to std::invalid_argument sees the same text.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tcb_internal.cuh"
+
+namespace tcb {
+
+ThreadState& state() {
+  static thread_local ThreadState st;
+  return st;
+}
+
+int set_error(int code, const std::string& msg) {
+  state().err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                  cudaGetErrorString(e) + ")";
+  return set_error(e == cudaErrorMemoryAllocation ? TCB_ENOMEM : TCB_ECUDA, m);
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = state().device < 0 ? 0 : state().device;
+  if (dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cached[dev] = n;
+  return n;
+}
+
+int ensure_init() {
+  ThreadState& st = state();
+  if (st.device >= 0) {
+    TCB_CUDA(cudaSetDevice(st.device));
+    return TCB_OK;
+  }
+  return tcb_init(0);
+}
+
+}  // namespace tcb
+
+using namespace tcb;
+
+#define TCB_TRY_INIT()              \
+  do {                              \
+    int rc_ = ensure_init();        \
+    if (rc_ != TCB_OK) return rc_;  \
+  } while (0)
+
+extern "C" {
+
+int tcb_init(int device) {
+  ThreadState& st = state();
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (n == 0) return set_error(TCB_ECUDA, "no CUDA device visible");
+  if (device < 0 || device >= n) return set_error(TCB_EINVAL, "tcb_init: device out of range");
+  TCB_CUDA(cudaSetDevice(device));
+  if (st.device != device) {
+    if (st.own_stream) cudaStreamDestroy(st.own_stream);
+    if (st.ev0) cudaEventDestroy(st.ev0);
+    if (st.ev1) cudaEventDestroy(st.ev1);
+    st.own_stream = nullptr;
+    st.ev0 = st.ev1 = nullptr;
+    st.ws = nullptr;
+    st.ws_bytes = 0;
+    st.counters = nullptr;
+    st.counters_n = 0;
+    TCB_CUDA(cudaStreamCreateWithFlags(&st.own_stream, cudaStreamNonBlocking));
+    TCB_CUDA(cudaEventCreate(&st.ev0));
+    TCB_CUDA(cudaEventCreate(&st.ev1));
+    st.stream = st.own_stream;
+    st.device = device;
+  }
+  return TCB_OK;
+}
+
+int tcb_finalize(void) {
+  ThreadState& st = state();
+  if (st.device < 0) return TCB_OK;
+  cudaSetDevice(st.device);
+  if (st.stream) cudaStreamSynchronize(st.stream);
+  if (st.ws) cudaFree(st.ws);
+  if (st.counters) cudaFree(st.counters);
+  if (st.own_stream) cudaStreamDestroy(st.own_stream);
+  if (st.ev0) cudaEventDestroy(st.ev0);
+  if (st.ev1) cudaEventDestroy(st.ev1);
+  st = ThreadState{};
+  return TCB_OK;
+}
+
+int tcb_device_count(int* count) {
+  if (!count) return set_error(TCB_EINVAL, "tcb_device_count: null pointer");
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return TCB_OK;
+}
+
+const char* tcb_last_error(void) { return state().err.c_str(); }
+
+int tcb_set_stream(void* stream) {
+  TCB_TRY_INIT();
+  ThreadState& st = state();
+  st.stream = stream ? static_cast<cudaStream_t>(stream) : st.own_stream;
+  return TCB_OK;
+}
+
+int tcb_sync(void) {
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaStreamSynchronize(state().stream));
+  return TCB_OK;
+}
+
+int tcb_alloc(void** dptr, int64_t bytes) {
+  TCB_TRY_INIT();
+  if (!dptr || bytes < 0) return set_error(TCB_EINVAL, "tcb_alloc: bad argument");
+  *dptr = nullptr;
+  if (bytes == 0) return TCB_OK;
+  TCB_CUDA(cudaMalloc(dptr, static_cast<size_t>(bytes)));
+  return TCB_OK;
+}
+
+int tcb_free(void* dptr) {
+  if (!dptr) return TCB_OK;
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaFree(dptr));
+  return TCB_OK;
+}
+
+int tcb_memset0(void* dptr, int64_t bytes) {
+  TCB_TRY_INIT();
+  if (bytes <= 0) return TCB_OK;
+  TCB_CUDA(cudaMemsetAsync(dptr, 0, static_cast<size_t>(bytes), state().stream));
+  return TCB_OK;
+}
+
+static int copy(void* dst, const void* src, int64_t bytes, cudaMemcpyKind kind) {
+  TCB_TRY_INIT();
+  if (bytes < 0) return set_error(TCB_EINVAL, "copy: negative size");
+  if (bytes == 0) return TCB_OK;
+  TCB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), kind, state().stream));
+  if (kind == cudaMemcpyDeviceToHost) TCB_CUDA(cudaStreamSynchronize(state().stream));
+  return TCB_OK;
+}
+
+int tcb_h2d(void* dst, const void* src, int64_t bytes) {
+  return copy(dst, src, bytes, cudaMemcpyHostToDevice);
+}
+int tcb_d2h(void* dst, const void* src, int64_t bytes) {
+  return copy(dst, src, bytes, cudaMemcpyDeviceToHost);
+}
+int tcb_d2d(void* dst, const void* src, int64_t bytes) {
+  return copy(dst, src, bytes, cudaMemcpyDeviceToDevice);
+}
+
+int tcb_host_register(void* ptr, int64_t bytes) {
+  TCB_TRY_INIT();
+  if (!ptr || bytes <= 0) return TCB_OK;
+  cudaError_t e = cudaHostRegister(ptr, static_cast<size_t>(bytes), cudaHostRegisterDefault);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return TCB_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaHostRegister");
+  return TCB_OK;
+}
+
+int tcb_host_unregister(void* ptr) {
+  TCB_TRY_INIT();
+  if (!ptr) return TCB_OK;
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e == cudaErrorHostMemoryNotRegistered) {
+    cudaGetLastError();
+    return TCB_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaHostUnregister");
+  return TCB_OK;
+}
+
+static int check_desc(const tcb_gemm_desc* d) {
+  if (!d) return set_error(TCB_EINVAL, "gemm: null descriptor");
+  if (d->m < 0 || d->n < 0 || d->k < 0) return set_error(TCB_EINVAL, "gemm: negative dimension");
+  if (d->c_nrow < 1 || d->c_nrow > TCB_MAX_DIMS || d->c_ncol < 1 || d->c_ncol > TCB_MAX_DIMS ||
+      d->nbatch < 0 || d->nbatch > TCB_MAX_DIMS)
+    return set_error(TCB_EUNSUPPORTED, "gemm: index-group rank outside [1, 6]");
+  int64_t pr = 1, pc = 1;
+  for (int i = 0; i < d->c_nrow; ++i) pr *= d->c_row_ext[i];
+  for (int i = 0; i < d->c_ncol; ++i) pc *= d->c_col_ext[i];
+  if (pr != d->m || pc != d->n)
+    return set_error(TCB_EINVAL, "gemm: output index groups do not cover m x n");
+  for (int i = 0; i < d->nbatch; ++i)
+    if (d->bat_ext[i] <= 0) return set_error(TCB_EINVAL, "gemm: batch extent must be positive");
+  return TCB_OK;
+}
+
+int tcb_gemm(const tcb_gemm_desc* d, const double* A, const double* B, double* C) {
+  TCB_TRY_INIT();
+  int rc = check_desc(d);
+  if (rc != TCB_OK) return rc;
+  ThreadState& st = state();
+  st.last_info = tcb_gemm_info{};
+  int64_t batch = 1;
+  for (int i = 0; i < d->nbatch; ++i) batch *= d->bat_ext[i];
+  if (d->m == 0 || d->n == 0 || batch == 0) return TCB_OK;
+  if (d->alpha == 0.0 || d->k == 0) {
+    if (d->beta == 1.0) return TCB_OK;
+    rc = launch_scale(*d, C);
+    st.last_info.launches = 1;
+    return rc;
+  }
+  if (d->n == 1 || d->m == 1) return launch_gemv(*d, A, B, C);
+  return launch_gemm(*d, A, B, C);
+}
+
+int tcb_last_gemm_info(tcb_gemm_info* info) {
+  if (!info) return set_error(TCB_EINVAL, "tcb_last_gemm_info: null pointer");
+  *info = state().last_info;
+  return TCB_OK;
+}
+
+// Reference argument checks, src/kernels_reference.cpp:12-24.
+static int check_blas(int ta, int tb, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb,
+                      int64_t ldc) {
+  if (m < 0 || n < 0 || k < 0) return set_error(TCB_EINVAL, "gemm: negative dimension");
+  const int64_t a_rows = ta ? k : m;
+  const int64_t b_rows = tb ? n : k;
+  if (lda < std::max<int64_t>(1, a_rows)) return set_error(TCB_EINVAL, "gemm: lda below row count");
+  if (ldb < std::max<int64_t>(1, b_rows)) return set_error(TCB_EINVAL, "gemm: ldb below row count");
+  if (ldc < std::max<int64_t>(1, m)) return set_error(TCB_EINVAL, "gemm: ldc below row count");
+  return TCB_OK;
+}
+
+static void blas_desc(tcb_gemm_desc* d, int ta, int tb, int64_t m, int64_t n, int64_t k,
+                      double alpha, int64_t lda, int64_t ldb, double beta, int64_t ldc) {
+  std::memset(d, 0, sizeof *d);
+  d->m = m;
+  d->n = n;
+  d->k = k;
+  d->a_sm = ta ? lda : 1;
+  d->a_sk = ta ? 1 : lda;
+  d->b_sk = tb ? ldb : 1;
+  d->b_sn = tb ? 1 : ldb;
+  d->c_nrow = d->c_ncol = 1;
+  d->c_row_ext[0] = m;
+  d->c_row_str[0] = 1;
+  d->c_col_ext[0] = n;
+  d->c_col_str[0] = ldc;
+  d->alpha = alpha;
+  d->beta = beta;
+}
+
+int tcb_dgemm(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+              int64_t ldc) {
+  int rc = check_blas(trans_a, trans_b, m, n, k, lda, ldb, ldc);
+  if (rc != TCB_OK) return rc;
+  tcb_gemm_desc d;
+  blas_desc(&d, trans_a, trans_b, m, n, k, alpha, lda, ldb, beta, ldc);
+  return tcb_gemm(&d, A, B, C);
+}
+
+int tcb_dgemm_strided_batched(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+                              double alpha, const double* A, int64_t lda, int64_t stride_a,
+                              const double* B, int64_t ldb, int64_t stride_b, double beta,
+                              double* C, int64_t ldc, int64_t stride_c, int64_t batch) {
+  int rc = check_blas(trans_a, trans_b, m, n, k, lda, ldb, ldc);
+  if (rc != TCB_OK) return rc;
+  if (batch < 0) return set_error(TCB_EINVAL, "gemm: negative batch count");
+  tcb_gemm_desc d;
+  blas_desc(&d, trans_a, trans_b, m, n, k, alpha, lda, ldb, beta, ldc);
+  d.nbatch = 1;
+  d.bat_ext[0] = batch;
+  d.bat_sa[0] = stride_a;
+  d.bat_sb[0] = stride_b;
+  d.bat_sc[0] = stride_c;
+  if (batch == 0) return TCB_OK;
+  return tcb_gemm(&d, A, B, C);
+}
+
+int tcb_dgemv(int trans, int64_t m, int64_t n, double alpha, const double* A, int64_t lda,
+              const double* x, int64_t incx, double beta, double* y, int64_t incy) {
+  // Reference checks, src/kernels_reference.cpp:84-86.
+  if (m < 0 || n < 0) return set_error(TCB_EINVAL, "gemv: negative dimension");
+  if (lda < std::max<int64_t>(1, m)) return set_error(TCB_EINVAL, "gemv: lda below row count");
+  tcb_gemm_desc d;
+  std::memset(&d, 0, sizeof d);
+  // y(len ylen) = op(A) x : as an (ylen x 1) = (ylen x xlen)(xlen x 1) product
+  const int64_t ylen = trans ? n : m, xlen = trans ? m : n;
+  d.m = ylen;
+  d.n = 1;
+  d.k = xlen;
+  d.a_sm = trans ? lda : 1;
+  d.a_sk = trans ? 1 : lda;
+  d.b_sk = incx;
+  d.b_sn = 1;
+  d.c_nrow = d.c_ncol = 1;
+  d.c_row_ext[0] = ylen;
+  d.c_row_str[0] = incy;
+  d.c_col_ext[0] = 1;
+  d.c_col_str[0] = 1;
+  d.alpha = alpha;
+  d.beta = beta;
+  return tcb_gemm(&d, A, x, y);
+}
+
+int tcb_dger(int64_t m, int64_t n, double alpha, const double* x, int64_t incx, const double* y,
+             int64_t incy, double* A, int64_t lda) {
+  // Reference checks, src/kernels_reference.cpp:125-127.
+  if (m < 0 || n < 0) return set_error(TCB_EINVAL, "ger: negative dimension");
+  if (lda < std::max<int64_t>(1, m)) return set_error(TCB_EINVAL, "ger: lda below row count");
+  if (alpha == 0.0) return TCB_OK;
+  tcb_gemm_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.m = m;
+  d.n = n;
+  d.k = 1;
+  d.a_sm = incx;
+  d.a_sk = 1;
+  d.b_sk = 1;
+  d.b_sn = incy;
+  d.c_nrow = d.c_ncol = 1;
+  d.c_row_ext[0] = m;
+  d.c_row_str[0] = 1;
+  d.c_col_ext[0] = n;
+  d.c_col_str[0] = lda;
+  d.alpha = alpha;
+  d.beta = 1.0;
+  return tcb_gemm(&d, x, y, A);
+}
+
+int tcb_ddot(int64_t k, const double* x, int64_t incx, const double* y, int64_t incy,
+             double* result_host) {
+  TCB_TRY_INIT();
+  if (!result_host) return set_error(TCB_EINVAL, "dot: null result pointer");
+  *result_host = 0.0;
+  if (k <= 0) return TCB_OK;
+  ThreadState& st = state();
+  double* dres = nullptr;
+  TCB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dres), 8, st.stream));
+  tcb_gemm_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.m = 1;
+  d.n = 1;
+  d.k = k;
+  d.a_sm = 1;
+  d.a_sk = incx;
+  d.b_sk = incy;
+  d.b_sn = 1;
+  d.c_nrow = d.c_ncol = 1;
+  d.c_row_ext[0] = d.c_col_ext[0] = 1;
+  d.c_row_str[0] = d.c_col_str[0] = 1;
+  d.alpha = 1.0;
+  d.beta = 0.0;
+  int rc = tcb_gemm(&d, x, y, dres);
+  if (rc == TCB_OK) {
+    cudaError_t e = cudaMemcpyAsync(result_host, dres, 8, cudaMemcpyDeviceToHost, st.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st.stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "dot result copy");
+  }
+  cudaFreeAsync(dres, st.stream);
+  return rc;
+}
+
+int tcb_permute(int rank, const int64_t* ext, const int64_t* src_str, const double* src,
+                double* dst) {
+  TCB_TRY_INIT();
+  if (rank < 0 || (rank > 0 && (!ext || !src_str)))
+    return set_error(TCB_EINVAL, "permute: bad argument");
+  return launch_permute(rank, ext, src_str, src, dst);
+}
+
+int tcb_timer_start(void) {
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaEventRecord(state().ev0, state().stream));
+  return TCB_OK;
+}
+
+int tcb_timer_stop(float* ms) {
+  TCB_TRY_INIT();
+  ThreadState& st = state();
+  TCB_CUDA(cudaEventRecord(st.ev1, st.stream));
+  TCB_CUDA(cudaEventSynchronize(st.ev1));
+  float v = 0.f;
+  TCB_CUDA(cudaEventElapsedTime(&v, st.ev0, st.ev1));
+  if (ms) *ms = v;
+  return TCB_OK;
+}
+
+int64_t tcb_launch_count(void) { return state().launches; }
+void tcb_reset_launch_count(void) { state().launches = 0; }
+
+}  // extern "C"

@@ -1,0 +1,730 @@
+// k1/k2 — fp64 GEMM on the B200 DMMA tensor pipe (mma.sync f64 -> SASS
+// DMMA.8x8x4), TMA + mbarrier staging, persistent CTAs, deterministic split-K.
+//
+// Replaces the reference's ReferenceBackend::gemm (src/kernels_reference.cpp:
+// 33-79) *and* the loop-over-GEMM nest around it (src/executor.cpp:119-177):
+// one launch evaluates every free-label slice (batch dims) and every
+// contracted slice (flattened into K) of a contraction.
+//
+// Design (sm_100a; fp64 has no tcgen05 kind, so the tensor pipe is reached
+// through warp-level mma.sync, fed from shared memory):
+//   * CTA tile 128x128x16, 8 warps (2 x 4, warp tile 64x32 = 8x4 DMMA 8x8
+//     blocks, 32 independent accumulators/warp). No separate producer warp: a
+//     9th warp would cap registers at 168 (the register file is split per
+//     SM sub-partition) and spill the accumulators.
+//   * 6-stage smem ring (32 KB/stage) with full/empty mbarriers. Each k-block
+//     step refills the stage released two blocks earlier (4 blocks in
+//     flight): thread 0 issues cp.async.bulk.tensor (TMA, 128B swizzle) when
+//     both operands are TMA-legal, else all 256 threads issue zero-filling
+//     8-byte cp.async that arrive on the same mbarrier.
+//   * Two smem layouts per operand: "MN-major" (outer index contiguous in
+//     global: 8 boxes of 16(outer) x 16(k)) and "K-major" (k contiguous: one box
+//     of 16(k) x 128(outer)); both 128B-swizzled. The k-set of each DMMA k-step
+//     is {0,1,4,5}+{0,2,8,10}[j] instead of 4 consecutive k, which makes the
+//     fragment loads of *both* layouts exactly 2 wavefronts (conflict-free).
+//   * Persistent: grid = min(units, #SMs); the producer runs ahead across
+//     tile boundaries so the next tile's operands land during the epilogue.
+//   * Split-K for small M*N: every split writes its partial tile to a
+//     workspace; the last-arriving CTA sums the partials in split order
+//     (bit-reproducible run to run) and applies alpha/beta.
+//   * Epilogue writes C through composite row/column offsets (index groups),
+//     so interleaved output orders need no permutation pass.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "tcb_internal.cuh"
+
+namespace tcb {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int PREFETCH = STAGES - 2;  // refill lag of two blocks (see kernel)
+constexpr int NCW = 8;                 // compute warps
+constexpr int CTHREADS = NCW * 32;     // 256
+constexpr int STAGE_A = BM * BK * 8;   // 16 KB
+constexpr int STAGE_B = BN * BK * 8;   // 16 KB
+constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct Params {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t M, N, K;
+  int64_t a_so, a_sk, b_so, b_sk;  // operand strides along (outer, k)
+  int c_nrow, c_ncol;
+  int64_t c_row_ext[TCB_MAX_DIMS], c_row_str[TCB_MAX_DIMS];
+  int64_t c_col_ext[TCB_MAX_DIMS], c_col_str[TCB_MAX_DIMS];
+  int nbatch;
+  int64_t bat_ext[TCB_MAX_DIMS], bat_sa[TCB_MAX_DIMS], bat_sb[TCB_MAX_DIMS], bat_sc[TCB_MAX_DIMS];
+  double alpha, beta;
+  int tiles_m, tiles_n, splits, kblocks;
+  int64_t units;
+  double* ws;
+  unsigned* counters;
+  // TMA: tensor-map rank and which batch dims each map carries.
+  int a_rank, b_rank;
+  int a_bdim[3], b_bdim[3];
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, bool valid) {
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                         int rank, const int* c) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(bar)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(bar)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(bar)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+          : "memory");
+      break;
+  }
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------ smem layouts
+// Byte offset of element (o = outer index in [0,128), k in [0,16)) in a stage.
+template <bool KMAJOR>
+__device__ __forceinline__ uint32_t tile_off(int o, int k) {
+  if (KMAJOR)  // one 16(k) x 128(o) box: row = o (128 B), chunk = k/2 ^ (o%8)
+    return o * 128 + ((((k >> 1) ^ (o & 7))) << 4) + ((k & 1) << 3);
+  // 8 boxes of 16(o) x 16(k): box o/16, row = k (128 B), chunk = (o%16)/2 ^ (k%8)
+  return (o >> 4) * 2048 + k * 128 + (((((o & 15) >> 1) ^ (k & 7))) << 4) + ((o & 1) << 3);
+}
+
+// k index of lane-quad q in k-step j of a 16-wide k block (see header note).
+__device__ __forceinline__ constexpr int kstep_k(int j, int q) {
+  return (q & 1) | ((q >> 1) << 2) | ((j & 1) << 1) | ((j >> 1) << 3);
+}
+
+// ------------------------------------------------------------- unit decode
+struct Unit {
+  int64_t batch;
+  int tm, tn, split;
+};
+
+__device__ __forceinline__ Unit decode_unit(const Params& p, int64_t u) {
+  Unit r;
+  r.split = static_cast<int>(u % p.splits);
+  int64_t t = u / p.splits;
+  const int64_t per_batch = static_cast<int64_t>(p.tiles_m) * p.tiles_n;
+  r.batch = t / per_batch;
+  int64_t tt = t % per_batch;
+  // grouped raster: 8 m-tiles share each n-tile sweep (L2 reuse of B)
+  const int64_t group_span = 8LL * p.tiles_n;
+  const int64_t g = tt / group_span;
+  const int first_m = static_cast<int>(g * 8);
+  const int gsize = min(8, p.tiles_m - first_m);
+  const int64_t w = tt % group_span;
+  r.tm = first_m + static_cast<int>(w % gsize);
+  r.tn = static_cast<int>(w / gsize);
+  return r;
+}
+
+__device__ __forceinline__ void batch_offsets(const Params& p, int64_t b, int64_t& oa,
+                                              int64_t& ob, int64_t& oc, int* coords) {
+  oa = ob = oc = 0;
+  for (int i = 0; i < p.nbatch; ++i) {
+    const int64_t e = p.bat_ext[i];
+    const int64_t c = b % e;
+    b /= e;
+    coords[i] = static_cast<int>(c);
+    oa += c * p.bat_sa[i];
+    ob += c * p.bat_sb[i];
+    oc += c * p.bat_sc[i];
+  }
+}
+
+__device__ __forceinline__ int64_t composite(int64_t idx, int n, const int64_t* ext,
+                                             const int64_t* str) {
+  int64_t off = 0;
+  for (int i = 0; i < n - 1; ++i) {
+    off += (idx % ext[i]) * str[i];
+    idx /= ext[i];
+  }
+  return off + idx * str[n - 1];
+}
+
+// ------------------------------------------------------------------ kernel
+// Load-side iterator: walks the same (unit, k-block) sequence as the consumer
+// loop, PREFETCH blocks ahead, across unit boundaries.
+struct LoadIter {
+  int64_t u;
+  int kb, kb1;
+  int64_t m0, n0, oa, ob;
+  int bc[TCB_MAX_DIMS];
+  bool valid;
+
+  __device__ __forceinline__ void start_unit(const Params& p) {
+    valid = u < p.units;
+    if (!valid) return;
+    const Unit un = decode_unit(p, u);
+    int64_t oc;
+    batch_offsets(p, un.batch, oa, ob, oc, bc);
+    kb = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
+    kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
+    m0 = static_cast<int64_t>(un.tm) * BM;
+    n0 = static_cast<int64_t>(un.tn) * BN;
+  }
+  __device__ __forceinline__ void advance(const Params& p) {
+    if (!valid) return;
+    if (++kb == kb1) {
+      u += gridDim.x;
+      start_unit(p);
+    }
+  }
+};
+
+// Issue the loads of the iterator's current k-block into `stage` (signals
+// full[stage]). TMA: thread 0 only. cp.async: all 256 threads.
+template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA>
+__device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& tmA,
+                                            const CUtensorMap& tmB, const LoadIter& li,
+                                            uint32_t sA, uint32_t full, int tid) {
+  const int64_t k0 = static_cast<int64_t>(li.kb) * BK;
+  const uint32_t sB = sA + STAGE_A;
+  if (USE_TMA) {
+    if (tid != 0) return;
+    mbar_expect_tx(full, STAGE_BYTES);
+    int c[5];
+    for (int i = 0; i < p.a_rank - 2; ++i) c[2 + i] = li.bc[p.a_bdim[i]];
+    if (A_KMAJOR) {
+      c[0] = static_cast<int>(k0);
+      c[1] = static_cast<int>(li.m0);
+      tma_load(sA, &tmA, full, p.a_rank, c);
+    } else {
+      c[1] = static_cast<int>(k0);
+#pragma unroll
+      for (int i = 0; i < BM / 16; ++i) {
+        c[0] = static_cast<int>(li.m0 + 16 * i);
+        tma_load(sA + i * 2048, &tmA, full, p.a_rank, c);
+      }
+    }
+    for (int i = 0; i < p.b_rank - 2; ++i) c[2 + i] = li.bc[p.b_bdim[i]];
+    if (B_KMAJOR) {
+      c[0] = static_cast<int>(k0);
+      c[1] = static_cast<int>(li.n0);
+      tma_load(sB, &tmB, full, p.b_rank, c);
+    } else {
+      c[1] = static_cast<int>(k0);
+#pragma unroll
+      for (int i = 0; i < BN / 16; ++i) {
+        c[0] = static_cast<int>(li.n0 + 16 * i);
+        tma_load(sB + i * 2048, &tmB, full, p.b_rank, c);
+      }
+    }
+  } else {
+    const double* Ab = p.A + li.oa;
+    const double* Bb = p.B + li.ob;
+    // 2048 elements per operand tile, 8 per thread; the thread order follows
+    // the operand's unit-stride index so warps read contiguous global memory.
+#pragma unroll
+    for (int i = 0; i < (BM * BK) / CTHREADS; ++i) {
+      const int idx = tid + CTHREADS * i;
+      const int o = (p.a_so == 1) ? (idx & (BM - 1)) : (idx >> 4);
+      const int k = (p.a_so == 1) ? (idx >> 7) : (idx & 15);
+      const int64_t gm = li.m0 + o, gk = k0 + k;
+      const bool ok = gm < p.M && gk < p.K;
+      cp_async8(sA + tile_off<A_KMAJOR>(o, k), ok ? Ab + gm * p.a_so + gk * p.a_sk : p.A, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < (BN * BK) / CTHREADS; ++i) {
+      const int idx = tid + CTHREADS * i;
+      const int o = (p.b_so == 1) ? (idx & (BN - 1)) : (idx >> 4);
+      const int k = (p.b_so == 1) ? (idx >> 7) : (idx & 15);
+      const int64_t gn = li.n0 + o, gk = k0 + k;
+      const bool ok = gn < p.N && gk < p.K;
+      cp_async8(sB + tile_off<B_KMAJOR>(o, k), ok ? Bb + gn * p.b_so + gk * p.b_sk : p.B, ok);
+    }
+    cp_async_arrive_noinc(full);
+  }
+}
+
+template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA>
+__global__ void __launch_bounds__(CTHREADS, 1)
+    dgemm_dmma_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t full0 = smem_u32(bars);            // full[s]  = full0 + 8s
+  const uint32_t empty0 = smem_u32(bars + STAGES);  // empty[s] = empty0 + 8s
+  volatile unsigned* s_flag = reinterpret_cast<volatile unsigned*>(bars + 2 * STAGES);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, USE_TMA ? 1 : CTHREADS);
+      mbar_init(empty0 + 8 * s, NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (USE_TMA) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+  }
+  __syncthreads();
+
+  // ---- prologue: put the first PREFETCH k-blocks in flight
+  LoadIter li;
+  li.u = blockIdx.x;
+  li.start_unit(p);
+  uint32_t gload = 0;  // k-blocks issued by this CTA
+#pragma unroll 1
+  for (int i = 0; i < PREFETCH && li.valid; ++i) {
+    issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + (gload % STAGES) * STAGE_BYTES,
+                                             full0 + 8 * (gload % STAGES), tid);
+    ++gload;
+    li.advance(p);
+  }
+
+  const int wm = warp & 1, wn = warp >> 1;
+  const int r = lane >> 2, q = lane & 3;
+
+  // Per-thread swizzle offsets. tile_off splits into a warp-uniform part
+  // (compile-time im/in/j terms) and an XOR part that depends on the lane and
+  // on two bits of (j, im|in): precompute those 4 lane offsets per operand.
+  //   K-major : off[j]                = tile_off<true>(r, kstep_k(j, q))
+  //   MN-major: off[(j&1)|(half<<1)]  = tile_off<false>(half*8 + r, kstep_k(j&1, q))
+  uint32_t offA[4], offB[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    offA[c] = A_KMAJOR ? tile_off<true>(r, kstep_k(c, q))
+                       : tile_off<false>((c >> 1) * 8 + r, kstep_k(c & 1, q));
+    offB[c] = B_KMAJOR ? tile_off<true>(r, kstep_k(c, q))
+                       : tile_off<false>((c >> 1) * 8 + r, kstep_k(c & 1, q));
+  }
+
+  uint32_t gcons = 0;  // k-blocks consumed by this CTA
+#pragma unroll 1
+  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const Unit un = decode_unit(p, u);
+    const int kb0 = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
+    const int kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll 1
+    for (int kb = kb0; kb < kb1; ++kb) {
+      // refill: block gload reuses the stage released two blocks ago
+      if (li.valid) {
+        const uint32_t s = gload % STAGES;
+        if (USE_TMA) {
+          if (tid == 0) mbar_wait(empty0 + 8 * s, ((gload / STAGES) & 1) ^ 1);
+        } else {
+          mbar_wait(empty0 + 8 * s, ((gload / STAGES) & 1) ^ 1);
+        }
+        issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
+                                                 full0 + 8 * s, tid);
+        ++gload;
+        li.advance(p);
+      }
+      const uint32_t stage = gcons % STAGES;
+      mbar_wait(full0 + 8 * stage, (gcons / STAGES) & 1);
+      const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double a[8], b[4];
+#pragma unroll
+        for (int im = 0; im < 8; ++im) {
+          const uint32_t addr =
+              A_KMAJOR ? sA + (wm * 64 + im * 8) * 128 + offA[j]
+                       : sA + (wm * 4 + (im >> 1)) * 2048 + (j >> 1) * 1024 +
+                             offA[(j & 1) | ((im & 1) << 1)];
+          a[im] = lds64(addr);
+        }
+#pragma unroll
+        for (int in = 0; in < 4; ++in) {
+          const uint32_t addr =
+              B_KMAJOR ? sB + (wn * 32 + in * 8) * 128 + offB[j]
+                       : sB + (wn * 2 + (in >> 1)) * 2048 + (j >> 1) * 1024 +
+                             offB[(j & 1) | ((in & 1) << 1)];
+          b[in] = lds64(addr);
+        }
+#pragma unroll
+        for (int im = 0; im < 8; ++im)
+#pragma unroll
+          for (int in = 0; in < 4; ++in) dmma(acc[im][in], a[im], b[in]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+      ++gcons;
+    }
+
+    // ------------------------------ epilogue ------------------------------
+    int bc[TCB_MAX_DIMS];
+    int64_t oa, ob, oc;
+    batch_offsets(p, un.batch, oa, ob, oc, bc);
+    const int64_t mbase = static_cast<int64_t>(un.tm) * BM + wm * 64 + r;
+    const int64_t nbase = static_cast<int64_t>(un.tn) * BN + wn * 32 + 2 * q;
+
+    if (p.splits > 1) {
+      const int64_t tile = u / p.splits;
+      double* part = p.ws + (tile * p.splits + un.split) * static_cast<int64_t>(BM * BN);
+#pragma unroll
+      for (int im = 0; im < 8; ++im)
+#pragma unroll
+        for (int in = 0; in < 4; ++in) {
+          const int v = im * 4 + in;
+          __stcg(reinterpret_cast<double2*>(part) + v * CTHREADS + tid,
+                 make_double2(acc[im][in][0], acc[im][in][1]));
+        }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned prev = atomicAdd(p.counters + tile, 1u);
+        *s_flag = (prev == static_cast<unsigned>(p.splits - 1)) ? 1u : 0u;
+      }
+      __syncthreads();
+      const bool last = *s_flag != 0u;
+      __syncthreads();  // s_flag is reused by the next unit
+      if (!last) continue;  // not the last split of this tile
+      __threadfence();
+      const double* base = p.ws + tile * p.splits * static_cast<int64_t>(BM * BN);
+#pragma unroll
+      for (int im = 0; im < 8; ++im)
+#pragma unroll
+        for (int in = 0; in < 4; ++in) acc[im][in][0] = acc[im][in][1] = 0.0;
+#pragma unroll 1
+      for (int s = 0; s < p.splits; ++s) {
+        const double2* ps =
+            reinterpret_cast<const double2*>(base + s * static_cast<int64_t>(BM * BN));
+#pragma unroll
+        for (int im = 0; im < 8; ++im)
+#pragma unroll
+          for (int in = 0; in < 4; ++in) {
+            const double2 v = __ldcg(ps + (im * 4 + in) * CTHREADS + tid);
+            acc[im][in][0] += v.x;
+            acc[im][in][1] += v.y;
+          }
+      }
+      if (tid == 0) p.counters[tile] = 0u;  // re-arm for the next launch
+    }
+
+    int64_t coff[4][2];
+    bool cok[4][2];
+#pragma unroll
+    for (int in = 0; in < 4; ++in)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int64_t n = nbase + in * 8 + jj;
+        cok[in][jj] = n < p.N;
+        coff[in][jj] = cok[in][jj] ? composite(n, p.c_ncol, p.c_col_ext, p.c_col_str) : 0;
+      }
+    double* Cb = p.C + oc;
+#pragma unroll
+    for (int im = 0; im < 8; ++im) {
+      const int64_t m = mbase + im * 8;
+      if (m >= p.M) continue;
+      const int64_t roff = composite(m, p.c_nrow, p.c_row_ext, p.c_row_str);
+#pragma unroll
+      for (int in = 0; in < 4; ++in)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          if (!cok[in][jj]) continue;
+          double* dst = Cb + roff + coff[in][jj];
+          double v = p.alpha * acc[im][in][jj];
+          if (p.beta != 0.0) v += p.beta * *dst;
+          *dst = v;
+        }
+    }
+  }
+  if (!USE_TMA) asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// beta-only update (alpha == 0 or K == 0): C <- beta*C, or 0 when beta == 0
+// (reference semantics, src/kernels_reference.cpp:38-45).
+__global__ void scale_kernel(Params p) {
+  const int64_t total = p.M * p.N * [&] {
+    int64_t b = 1;
+    for (int i = 0; i < p.nbatch; ++i) b *= p.bat_ext[i];
+    return b;
+  }();
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = e % p.M, n = (e / p.M) % p.N, b = e / (p.M * p.N);
+    int bc[TCB_MAX_DIMS];
+    int64_t oa, ob, oc;
+    batch_offsets(p, b, oa, ob, oc, bc);
+    double* dst = p.C + oc + composite(m, p.c_nrow, p.c_row_ext, p.c_row_str) +
+                  composite(n, p.c_ncol, p.c_col_ext, p.c_col_str);
+    *dst = p.beta == 0.0 ? 0.0 : p.beta * *dst;
+  }
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// Build the tensor map of one operand: dims (outer, k) or (k, outer) plus the
+// batch dims whose stride is non-zero. Returns false when TMA cannot describe
+// the operand (alignment, strides, rank) — the caller then uses cp.async.
+bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t outer, int64_t K,
+              int64_t s_outer, int64_t s_k, const tcb_gemm_desc& d, const int64_t* bstr,
+              int* rank, int* bdim) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if (reinterpret_cast<uintptr_t>(base) % 16) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  const int64_t lead_ext = kmajor ? K : outer;
+  const int64_t other_ext = kmajor ? outer : K;
+  const int64_t other_str = kmajor ? s_outer : s_k;
+  if ((kmajor ? s_k : s_outer) != 1 && lead_ext > 1) return false;
+  if (lead_ext >= (1LL << 31) || other_ext >= (1LL << 31)) return false;
+  dims[0] = static_cast<cuuint64_t>(lead_ext);
+  dims[1] = static_cast<cuuint64_t>(other_ext);
+  box[0] = 16;
+  box[1] = kmajor ? 128 : 16;
+  int64_t os = other_ext > 1 ? other_str : 2;  // extent-1 dims: any legal stride
+  if (os <= 0 || os % 2 || os * 8 >= (1LL << 40)) return false;
+  strides[0] = static_cast<cuuint64_t>(os * 8);
+  int r = 2;
+  for (int i = 0; i < d.nbatch; ++i) {
+    if (bstr[i] == 0 || d.bat_ext[i] == 1) continue;
+    if (r == 5) return false;
+    if (bstr[i] < 0 || bstr[i] % 2 || bstr[i] * 8 >= (1LL << 40)) return false;
+    if (d.bat_ext[i] >= (1LL << 31)) return false;
+    dims[r] = static_cast<cuuint64_t>(d.bat_ext[i]);
+    strides[r - 1] = static_cast<cuuint64_t>(bstr[i] * 8);
+    box[r] = 1;
+    bdim[r - 2] = i;
+    ++r;
+  }
+  *rank = r;
+  const CUresult res =
+      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, r, const_cast<double*>(base), dims, strides, box,
+         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
+
+template <bool AK, bool BK_, bool TMA>
+cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap& tb, int grid,
+                       cudaStream_t s) {
+  auto kern = dgemm_dmma_kernel<AK, BK_, TMA>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, CTHREADS, SMEM_BYTES, s>>>(p, ta, tb);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_scale(const tcb_gemm_desc& d, double* C) {
+  Params p{};
+  p.C = C;
+  p.M = d.m;
+  p.N = d.n;
+  p.c_nrow = d.c_nrow;
+  p.c_ncol = d.c_ncol;
+  for (int i = 0; i < TCB_MAX_DIMS; ++i) {
+    p.c_row_ext[i] = d.c_row_ext[i];
+    p.c_row_str[i] = d.c_row_str[i];
+    p.c_col_ext[i] = d.c_col_ext[i];
+    p.c_col_str[i] = d.c_col_str[i];
+    p.bat_ext[i] = d.bat_ext[i];
+    p.bat_sa[i] = d.bat_sa[i];
+    p.bat_sb[i] = d.bat_sb[i];
+    p.bat_sc[i] = d.bat_sc[i];
+  }
+  p.nbatch = d.nbatch;
+  p.beta = d.beta;
+  scale_kernel<<<num_sms() * 4, 256, 0, state().stream>>>(p);
+  TCB_LAUNCHED();
+  return TCB_OK;
+}
+
+int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C) {
+  ThreadState& st = state();
+  Params p{};
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.M = d.m;
+  p.N = d.n;
+  p.K = d.k;
+  p.a_so = d.a_sm;
+  p.a_sk = d.a_sk;
+  p.b_so = d.b_sn;
+  p.b_sk = d.b_sk;
+  p.c_nrow = d.c_nrow;
+  p.c_ncol = d.c_ncol;
+  int64_t batch = 1;
+  for (int i = 0; i < TCB_MAX_DIMS; ++i) {
+    p.c_row_ext[i] = d.c_row_ext[i];
+    p.c_row_str[i] = d.c_row_str[i];
+    p.c_col_ext[i] = d.c_col_ext[i];
+    p.c_col_str[i] = d.c_col_str[i];
+    p.bat_ext[i] = d.bat_ext[i];
+    p.bat_sa[i] = d.bat_sa[i];
+    p.bat_sb[i] = d.bat_sb[i];
+    p.bat_sc[i] = d.bat_sc[i];
+  }
+  p.nbatch = d.nbatch;
+  for (int i = 0; i < d.nbatch; ++i) batch *= d.bat_ext[i];
+  p.alpha = d.alpha;
+  p.beta = d.beta;
+  p.tiles_m = static_cast<int>((d.m + BM - 1) / BM);
+  p.tiles_n = static_cast<int>((d.n + BN - 1) / BN);
+  const int64_t kblocks = (d.k + BK - 1) / BK;
+  if (kblocks >= (1LL << 31)) return set_error(TCB_EUNSUPPORTED, "gemm: K too large");
+  p.kblocks = static_cast<int>(kblocks);
+  const int64_t tiles = batch * p.tiles_m * p.tiles_n;
+  const int sms = num_sms();
+
+  // Split-K when the tile grid leaves most SMs idle (cfg1-type shapes).
+  int splits = 1;
+  if (tiles < sms) {
+    splits = static_cast<int>(std::min<int64_t>(sms / tiles, std::max<int64_t>(1, kblocks / 8)));
+    splits = std::max(1, splits);
+  }
+  p.splits = splits;
+  p.units = tiles * splits;
+
+  if (splits > 1) {
+    const int64_t need = tiles * splits * BM * BN * 8;
+    if (need > st.ws_bytes) {
+      if (st.ws) cudaFree(st.ws);
+      st.ws = nullptr;
+      st.ws_bytes = 0;
+      TCB_CUDA(cudaMalloc(&st.ws, need));
+      st.ws_bytes = need;
+    }
+    if (tiles > st.counters_n) {
+      if (st.counters) cudaFree(st.counters);
+      st.counters = nullptr;
+      st.counters_n = 0;
+      TCB_CUDA(cudaMalloc(&st.counters, tiles * sizeof(unsigned)));
+      TCB_CUDA(cudaMemsetAsync(st.counters, 0, tiles * sizeof(unsigned), st.stream));
+      st.counters_n = tiles;
+    }
+    p.ws = static_cast<double*>(st.ws);
+    p.counters = st.counters;
+  }
+
+  // Operand layouts: MN-major when the outer index is unit-stride.
+  const bool a_k = !(p.a_so == 1 || d.m == 1) && (p.a_sk == 1);
+  const bool b_k = !(p.b_so == 1 || d.n == 1) && (p.b_sk == 1);
+  CUtensorMap ta, tb;
+  std::memset(&ta, 0, sizeof ta);
+  std::memset(&tb, 0, sizeof tb);
+  bool tma = make_map(&ta, A, a_k, d.m, d.k, p.a_so, p.a_sk, d, d.bat_sa, &p.a_rank, p.a_bdim) &&
+             make_map(&tb, B, b_k, d.n, d.k, p.b_so, p.b_sk, d, d.bat_sb, &p.b_rank, p.b_bdim);
+  // MN-major layout needs unit outer stride for TMA; K-major needs unit k stride.
+  if (tma && !a_k && p.a_so != 1 && d.m > 1) tma = false;
+  if (tma && !b_k && p.b_so != 1 && d.n > 1) tma = false;
+
+  const int grid = static_cast<int>(std::min<int64_t>(p.units, sms));
+  cudaError_t e;
+  if (tma) {
+    if (a_k && b_k) e = launch_one<true, true, true>(p, ta, tb, grid, st.stream);
+    else if (a_k) e = launch_one<true, false, true>(p, ta, tb, grid, st.stream);
+    else if (b_k) e = launch_one<false, true, true>(p, ta, tb, grid, st.stream);
+    else e = launch_one<false, false, true>(p, ta, tb, grid, st.stream);
+  } else {
+    if (a_k && b_k) e = launch_one<true, true, false>(p, ta, tb, grid, st.stream);
+    else if (a_k) e = launch_one<true, false, false>(p, ta, tb, grid, st.stream);
+    else if (b_k) e = launch_one<false, true, false>(p, ta, tb, grid, st.stream);
+    else e = launch_one<false, false, false>(p, ta, tb, grid, st.stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "dgemm_dmma launch");
+  ++st.launches;
+  st.last_info.path = tma ? 0 : 1;
+  st.last_info.splits = splits;
+  st.last_info.units = p.units;
+  st.last_info.grid = grid;
+  st.last_info.launches = 1;
+  return TCB_OK;
+}
+
+}  // namespace tcb

@@ -1,0 +1,56 @@
+// Internal helpers shared by the device translation units of libtcb200.so.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "tcb.h"
+
+namespace tcb {
+
+// Per host-thread state: the device this thread drives, its stream, a grow-only
+// workspace (split-K partials + per-tile counters) and the last error text.
+struct ThreadState {
+  int device = -1;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // own_stream or a caller stream
+  void* ws = nullptr;             // split-K partials
+  int64_t ws_bytes = 0;
+  unsigned* counters = nullptr;   // per-tile arrival counters (kept zeroed)
+  int64_t counters_n = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+  tcb_gemm_info last_info{};
+  std::string err;
+};
+
+ThreadState& state();
+int set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int ensure_init();  // lazily binds device 0 when tcb_init was not called
+
+#define TCB_CUDA(call)                                        \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return ::tcb::cuda_fail(e_, #call); \
+  } while (0)
+
+#define TCB_LAUNCHED()                                                       \
+  do {                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                     \
+    if (e_ != cudaSuccess) return ::tcb::cuda_fail(e_, "kernel launch");     \
+    ++::tcb::state().launches;                                               \
+  } while (0)
+
+// Device-side launchers (implemented in the .cu files).
+int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C);
+int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const double* src,
+                   double* dst);
+int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double* C);
+int launch_scale(const tcb_gemm_desc& d, double* C);
+int num_sms();
+
+}  // namespace tcb

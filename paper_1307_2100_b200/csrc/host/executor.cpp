@@ -1,0 +1,369 @@
+// L3/L4 on the device: the "b200" KernelBackend and the plan executor.
+//
+// The reference executor walks the plan's loop nest and issues one CPU BLAS
+// call per slice (src/executor.cpp:287-369, run_range :102-283). Here the
+// contraction is lowered once (lower.cpp) and executed as permutations + one
+// device launch through the C-ABI (tcb.h). Host C++ only: no CUDA headers.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+
+#include "tc/contract.hpp"
+#include "tcb.h"
+
+namespace tc {
+namespace {
+
+// Map a C-ABI status to the reference's exception types.
+void check(int status, const char* what) {
+  if (status == TCB_OK) return;
+  std::string msg = tcb_last_error();
+  if (msg.empty()) msg = what;
+  if (status == TCB_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(std::string(what) + ": " + msg);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(std::int64_t bytes) { check(tcb_alloc(&p, bytes), "device allocation"); }
+  ~DevBuf() { tcb_free(p); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  double* d() const { return static_cast<double*>(p); }
+};
+
+class B200Backend final : public KernelBackend {
+ public:
+  explicit B200Backend(const B200Options& o) : opt_(o) {}
+  const std::string& name() const override {
+    static const std::string n = "b200";
+    return n;
+  }
+  const B200Options& options() const { return opt_; }
+
+  // Fault injection (B200Options::fail_after_launches).
+  void tick(const char* where) const {
+    if (opt_.fail_after_launches < 0) return;
+    std::lock_guard<std::mutex> g(mu_);
+    if (ops_++ >= opt_.fail_after_launches)
+      throw std::runtime_error(std::string("synthetic device fault in ") + where);
+  }
+
+  void gemm(bool ta, bool tb, std::int64_t m, std::int64_t n, std::int64_t k, double alpha,
+            const double* a, std::int64_t lda, const double* b, std::int64_t ldb, double beta,
+            double* c, std::int64_t ldc) const override {
+    check(tcb_init(opt_.device), "tcb_init");
+    // validate with the device layer's reference-compatible checks first
+    const std::int64_t a_rows = ta ? k : m, a_cols = ta ? m : k;
+    const std::int64_t b_rows = tb ? n : k, b_cols = tb ? k : n;
+    if (m < 0 || n < 0 || k < 0) throw std::invalid_argument("gemm: negative dimension");
+    if (lda < std::max<std::int64_t>(1, a_rows)) throw std::invalid_argument("gemm: lda below row count");
+    if (ldb < std::max<std::int64_t>(1, b_rows)) throw std::invalid_argument("gemm: ldb below row count");
+    if (ldc < std::max<std::int64_t>(1, m)) throw std::invalid_argument("gemm: ldc below row count");
+    tick("gemm");
+    if (m == 0 || n == 0) return;
+    const std::int64_t na = a_cols > 0 ? lda * (a_cols - 1) + a_rows : 0;
+    const std::int64_t nb = b_cols > 0 ? ldb * (b_cols - 1) + b_rows : 0;
+    const std::int64_t nc = ldc * (n - 1) + m;
+    DevBuf da(std::max<std::int64_t>(na, 1) * 8), db(std::max<std::int64_t>(nb, 1) * 8),
+        dc(nc * 8);
+    if (na) check(tcb_h2d(da.p, a, na * 8), "gemm upload");
+    if (nb) check(tcb_h2d(db.p, b, nb * 8), "gemm upload");
+    check(tcb_h2d(dc.p, c, nc * 8), "gemm upload");
+    check(tcb_dgemm(ta, tb, m, n, k, alpha, da.d(), lda, db.d(), ldb, beta, dc.d(), ldc), "gemm");
+    check(tcb_d2h(c, dc.p, nc * 8), "gemm download");
+  }
+
+  void gemv(bool trans, std::int64_t m, std::int64_t n, double alpha, const double* a,
+            std::int64_t lda, const double* x, std::int64_t incx, double beta, double* y,
+            std::int64_t incy) const override {
+    check(tcb_init(opt_.device), "tcb_init");
+    if (m < 0 || n < 0) throw std::invalid_argument("gemv: negative dimension");
+    if (lda < std::max<std::int64_t>(1, m)) throw std::invalid_argument("gemv: lda below row count");
+    tick("gemv");
+    const std::int64_t ylen = trans ? n : m, xlen = trans ? m : n;
+    if (ylen == 0) return;
+    const std::int64_t na = n > 0 ? lda * (n - 1) + m : 0;
+    const std::int64_t nx = xlen > 0 ? (xlen - 1) * std::abs(incx) + 1 : 0;
+    const std::int64_t ny = (ylen - 1) * std::abs(incy) + 1;
+    DevBuf da(std::max<std::int64_t>(na, 1) * 8), dx(std::max<std::int64_t>(nx, 1) * 8),
+        dy(ny * 8);
+    if (na) check(tcb_h2d(da.p, a, na * 8), "gemv upload");
+    if (nx) check(tcb_h2d(dx.p, x, nx * 8), "gemv upload");
+    check(tcb_h2d(dy.p, y, ny * 8), "gemv upload");
+    check(tcb_dgemv(trans, m, n, alpha, da.d(), lda, dx.d(), incx, beta, dy.d(), incy), "gemv");
+    check(tcb_d2h(y, dy.p, ny * 8), "gemv download");
+  }
+
+  void ger(std::int64_t m, std::int64_t n, double alpha, const double* x, std::int64_t incx,
+           const double* y, std::int64_t incy, double* a, std::int64_t lda) const override {
+    check(tcb_init(opt_.device), "tcb_init");
+    if (m < 0 || n < 0) throw std::invalid_argument("ger: negative dimension");
+    if (lda < std::max<std::int64_t>(1, m)) throw std::invalid_argument("ger: lda below row count");
+    tick("ger");
+    if (m == 0 || n == 0 || alpha == 0.0) return;
+    const std::int64_t nx = (m - 1) * std::abs(incx) + 1, ny = (n - 1) * std::abs(incy) + 1;
+    const std::int64_t na = lda * (n - 1) + m;
+    DevBuf dx(nx * 8), dy(ny * 8), da(na * 8);
+    check(tcb_h2d(dx.p, x, nx * 8), "ger upload");
+    check(tcb_h2d(dy.p, y, ny * 8), "ger upload");
+    check(tcb_h2d(da.p, a, na * 8), "ger upload");
+    check(tcb_dger(m, n, alpha, dx.d(), incx, dy.d(), incy, da.d(), lda), "ger");
+    check(tcb_d2h(a, da.p, na * 8), "ger download");
+  }
+
+  double dot(std::int64_t k, const double* x, std::int64_t incx, const double* y,
+             std::int64_t incy) const override {
+    check(tcb_init(opt_.device), "tcb_init");
+    tick("dot");
+    if (k <= 0) return 0.0;
+    const std::int64_t nx = (k - 1) * std::abs(incx) + 1, ny = (k - 1) * std::abs(incy) + 1;
+    DevBuf dx(nx * 8), dy(ny * 8);
+    check(tcb_h2d(dx.p, x, nx * 8), "dot upload");
+    check(tcb_h2d(dy.p, y, ny * 8), "dot upload");
+    double r = 0.0;
+    check(tcb_ddot(k, dx.d(), incx, dy.d(), incy, &r), "dot");
+    return r;
+  }
+
+ private:
+  B200Options opt_;
+  mutable std::mutex mu_;
+  mutable int ops_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<KernelBackend> make_b200_backend(const B200Options& options) {
+  return std::make_unique<B200Backend>(options);
+}
+
+std::unique_ptr<KernelBackend> make_backend(const std::string& name) {
+  if (name == "b200" || name == "device") return make_b200_backend();
+  if (name == "reference" || name == "external")
+    throw std::invalid_argument("backend '" + name +
+                                "' is a CPU backend of the reference engine; this engine runs on "
+                                "the B200: use make_backend(\"b200\")");
+  throw std::invalid_argument("unknown backend '" + name + "'");
+}
+
+// --------------------------------------------------------- PreparedContraction
+
+PreparedContraction::PreparedContraction(const ValidatedContraction& v, int device)
+    : recipe_(lower(v)), device_(device) {
+  check(tcb_init(device_), "tcb_init");
+  nl_ = 1;
+  for (int m = 0; m < v.left_rank(); ++m) nl_ *= v.label_at_left_mode(m).extent;
+  nr_ = 1;
+  for (int m = 0; m < v.right_rank(); ++m) nr_ *= v.label_at_right_mode(m).extent;
+  no_ = 1;
+  for (std::int64_t e : v.output_extents()) no_ *= e;
+  if (recipe_.row_ext.size() > TCB_MAX_DIMS || recipe_.col_ext.size() > TCB_MAX_DIMS ||
+      recipe_.bat_ext.size() > TCB_MAX_DIMS)
+    throw std::invalid_argument("contraction needs more than 6 index groups per role");
+  void* p = nullptr;
+  try {
+    check(tcb_alloc(&p, nl_ * 8), "device allocation");
+    dl_ = static_cast<double*>(p);
+    check(tcb_alloc(&p, nr_ * 8), "device allocation");
+    dr_ = static_cast<double*>(p);
+    check(tcb_alloc(&p, no_ * 8), "device allocation");
+    do_ = static_cast<double*>(p);
+    for (const PermuteStep& ps : recipe_.permutes) {
+      check(tcb_alloc(&p, ps.elements * 8), "device allocation");
+      (ps.right ? pr_ : pl_) = static_cast<double*>(p);
+    }
+  } catch (...) {
+    tcb_free(dl_);
+    tcb_free(dr_);
+    tcb_free(do_);
+    tcb_free(pl_);
+    tcb_free(pr_);
+    throw;
+  }
+}
+
+PreparedContraction::~PreparedContraction() {
+  tcb_init(device_);
+  tcb_sync();
+  tcb_free(dl_);
+  tcb_free(dr_);
+  tcb_free(do_);
+  tcb_free(pl_);
+  tcb_free(pr_);
+}
+
+std::int64_t PreparedContraction::permuted_bytes() const {
+  std::int64_t b = 0;
+  for (const PermuteStep& ps : recipe_.permutes) b += ps.elements * 8;
+  return b;
+}
+
+void PreparedContraction::upload(const double* left, const double* right) {
+  check(tcb_init(device_), "tcb_init");
+  check(tcb_h2d(dl_, left, nl_ * 8), "upload");
+  check(tcb_h2d(dr_, right, nr_ * 8), "upload");
+}
+
+void PreparedContraction::run() {
+  check(tcb_init(device_), "tcb_init");
+  const std::int64_t before = tcb_launch_count();
+  const double* a = dl_;
+  const double* b = dr_;
+  for (const PermuteStep& ps : recipe_.permutes) {
+    double* dst = ps.right ? pr_ : pl_;
+    check(tcb_permute(static_cast<int>(ps.ext.size()), ps.ext.data(), ps.src_str.data(),
+                      ps.right ? dr_ : dl_, dst),
+          "permute");
+    (ps.right ? b : a) = dst;
+  }
+  tcb_gemm_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.m = recipe_.m;
+  d.n = recipe_.n;
+  d.k = recipe_.k;
+  d.a_sm = recipe_.a_sm;
+  d.a_sk = recipe_.a_sk;
+  d.b_sk = recipe_.b_sk;
+  d.b_sn = recipe_.b_sn;
+  d.c_nrow = static_cast<int32_t>(recipe_.row_ext.size());
+  d.c_ncol = static_cast<int32_t>(recipe_.col_ext.size());
+  for (std::size_t i = 0; i < recipe_.row_ext.size(); ++i) {
+    d.c_row_ext[i] = recipe_.row_ext[i];
+    d.c_row_str[i] = recipe_.row_str[i];
+  }
+  for (std::size_t i = 0; i < recipe_.col_ext.size(); ++i) {
+    d.c_col_ext[i] = recipe_.col_ext[i];
+    d.c_col_str[i] = recipe_.col_str[i];
+  }
+  d.nbatch = static_cast<int32_t>(recipe_.bat_ext.size());
+  for (std::size_t i = 0; i < recipe_.bat_ext.size(); ++i) {
+    d.bat_ext[i] = recipe_.bat_ext[i];
+    d.bat_sa[i] = recipe_.bat_sa[i];
+    d.bat_sb[i] = recipe_.bat_sb[i];
+    d.bat_sc[i] = recipe_.bat_sc[i];
+  }
+  d.alpha = 1.0;
+  d.beta = 0.0;
+  check(tcb_gemm(&d, a, b, do_), "contraction");
+  launches_ = tcb_launch_count() - before;
+}
+
+void PreparedContraction::download(double* out) {
+  check(tcb_init(device_), "tcb_init");
+  check(tcb_d2h(out, do_, no_ * 8), "download");
+}
+
+void PreparedContraction::sync() {
+  check(tcb_init(device_), "tcb_init");
+  check(tcb_sync(), "sync");
+}
+
+// ------------------------------------------------------------------ execute
+
+std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
+                                          const ValidatedContraction& v, const Tensor& left,
+                                          const Tensor& right, const KernelBackend& backend,
+                                          int workers) {
+  (void)workers;  // one device launch; the result does not depend on it
+  // plan/operand consistency (reference: src/executor.cpp:292-303)
+  if (plan.label_extents.size() != v.labels.size())
+    throw std::invalid_argument("plan does not match contraction");
+  for (std::size_t i = 0; i < v.labels.size(); ++i) {
+    const LabelInfo& li = v.labels[i];
+    if (li.extent != plan.label_extents[i])
+      throw std::invalid_argument("extent drift between planning and execution on label '" +
+                                  li.label + "'");
+    if (li.left_mode >= 0 && left.extent(li.left_mode) != li.extent)
+      throw std::invalid_argument("left operand extent drift on label '" + li.label + "'");
+    if (li.right_mode >= 0 && right.extent(li.right_mode) != li.extent)
+      throw std::invalid_argument("right operand extent drift on label '" + li.label + "'");
+  }
+  const auto* dev = dynamic_cast<const B200Backend*>(&backend);
+  if (!dev)
+    throw std::invalid_argument("execute: backend '" + backend.name() +
+                                "' has no device path; use tc::make_backend(\"b200\")");
+
+  const auto t0 = std::chrono::steady_clock::now();
+  Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name);
+  ExecutionStats st;
+  st.flops = plan.flops;
+  try {
+    dev->tick("execute");
+    PreparedContraction pc(v, dev->options().device);
+    pc.upload(left.data(), right.data());
+    pc.run();
+    pc.download(out.data());
+    st.kernel_calls = pc.launches_last_run();
+    st.packed_bytes = pc.permuted_bytes();
+  } catch (const std::invalid_argument&) {
+    throw;
+  } catch (const std::exception& e) {
+    throw std::runtime_error(std::string(e.what()) + " while executing " +
+                             lower(v).summary() + " for " + unparse(v.spec));
+  }
+  st.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return {std::move(out), st};
+}
+
+std::vector<SlicingRun> execute_all_slicings(const ValidatedContraction& v, const Tensor& left,
+                                             const Tensor& right, const KernelBackend& backend,
+                                             std::int64_t work_cap) {
+  const std::vector<SlicingOption> opts = enumerate_slicings(v);
+  const std::int64_t macs = flop_count(v) / 2;
+  if (macs * static_cast<std::int64_t>(opts.size()) > work_cap)
+    throw resource_limit_error("slicing sweep work exceeds cap");
+  std::vector<SlicingRun> runs;
+  runs.reserve(opts.size());
+  for (const SlicingOption& o : opts) {
+    SlicingRun run;
+    run.s_left = o.s_left;
+    run.s_right = o.s_right;
+    run.kernel = o.report.kernel;
+    const ExecutionPlan p = plan(v, PlanPolicy::force_slicing(o.s_left, o.s_right));
+    auto [res, st] = execute(p, v, left, right, backend);
+    run.result_hash = tensor_hash(res);
+    run.stats = st;
+    run.result = std::move(res);
+    runs.push_back(std::move(run));
+  }
+  return runs;
+}
+
+std::uint64_t tensor_hash(const Tensor& t) {
+  // FNV-1a over the little-endian bytes of each element (src/executor.cpp:371-383)
+  std::uint64_t h = 0xcbf29ce484222325ull;
+  const unsigned char* bytes = reinterpret_cast<const unsigned char*>(t.data());
+  const std::size_t n = static_cast<std::size_t>(t.size()) * sizeof(double);
+  for (std::size_t i = 0; i < n; ++i) {
+    h ^= bytes[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+double max_rel_error(const Tensor& a, const Tensor& b) {
+  if (a.size() != b.size()) return std::numeric_limits<double>::infinity();
+  double scale = 1.0, worst = 0.0;
+  for (std::int64_t i = 0; i < b.size(); ++i) scale = std::max(scale, std::fabs(b.data()[i]));
+  for (std::int64_t i = 0; i < a.size(); ++i)
+    worst = std::max(worst, std::fabs(a.data()[i] - b.data()[i]));
+  return worst / scale;
+}
+
+double rel_frobenius_error(const Tensor& a, const Tensor& b) {
+  if (a.size() != b.size()) return std::numeric_limits<double>::infinity();
+  long double num = 0, den = 0;
+  for (std::int64_t i = 0; i < a.size(); ++i) {
+    const long double d = static_cast<long double>(a.data()[i]) - b.data()[i];
+    num += d * d;
+    den += static_cast<long double>(b.data()[i]) * b.data()[i];
+  }
+  if (den == 0) return num == 0 ? 0.0 : std::numeric_limits<double>::infinity();
+  return static_cast<double>(std::sqrt(num / den));
+}
+
+}  // namespace tc

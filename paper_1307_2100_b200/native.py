@@ -1,0 +1,133 @@
+"""ctypes bindings of the engine's two C-ABIs (include/tcb.h, include/tcf.h).
+
+There is no fallback: if the in-tree libraries are missing this module builds
+them (nvcc/g++ are in the image) and raises if that fails. Nothing here calls
+the CPU oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB = PKG / "lib"
+
+_lock = threading.Lock()
+_libs: dict[str, C.CDLL] = {}
+
+i64, i32, f64, vp, cp = C.c_int64, C.c_int, C.c_double, C.c_void_p, C.c_char_p
+P_i64 = C.POINTER(C.c_int64)
+P_f64 = C.POINTER(C.c_double)
+TCB_MAX_DIMS = 6
+
+
+class GemmDesc(C.Structure):
+    """tcb_gemm_desc (include/tcb.h)."""
+    _fields_ = [("m", i64), ("n", i64), ("k", i64),
+                ("a_sm", i64), ("a_sk", i64), ("b_sk", i64), ("b_sn", i64),
+                ("c_nrow", C.c_int32), ("c_ncol", C.c_int32),
+                ("c_row_ext", i64 * TCB_MAX_DIMS), ("c_row_str", i64 * TCB_MAX_DIMS),
+                ("c_col_ext", i64 * TCB_MAX_DIMS), ("c_col_str", i64 * TCB_MAX_DIMS),
+                ("nbatch", C.c_int32),
+                ("bat_ext", i64 * TCB_MAX_DIMS), ("bat_sa", i64 * TCB_MAX_DIMS),
+                ("bat_sb", i64 * TCB_MAX_DIMS), ("bat_sc", i64 * TCB_MAX_DIMS),
+                ("alpha", f64), ("beta", f64)]
+
+
+class GemmInfo(C.Structure):
+    _fields_ = [("path", C.c_int32), ("splits", C.c_int32), ("units", i64),
+                ("grid", C.c_int32), ("launches", C.c_int32)]
+
+
+# name -> (restype, argtypes)
+TCB_API = {
+    "tcb_init": (i32, [i32]),
+    "tcb_finalize": (i32, []),
+    "tcb_device_count": (i32, [C.POINTER(C.c_int)]),
+    "tcb_last_error": (cp, []),
+    "tcb_set_stream": (i32, [vp]),
+    "tcb_sync": (i32, []),
+    "tcb_alloc": (i32, [C.POINTER(vp), i64]),
+    "tcb_free": (i32, [vp]),
+    "tcb_memset0": (i32, [vp, i64]),
+    "tcb_h2d": (i32, [vp, vp, i64]),
+    "tcb_d2h": (i32, [vp, vp, i64]),
+    "tcb_d2d": (i32, [vp, vp, i64]),
+    "tcb_host_register": (i32, [vp, i64]),
+    "tcb_host_unregister": (i32, [vp]),
+    "tcb_gemm": (i32, [C.POINTER(GemmDesc), vp, vp, vp]),
+    "tcb_last_gemm_info": (i32, [C.POINTER(GemmInfo)]),
+    "tcb_dgemm": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64]),
+    "tcb_dgemm_strided_batched": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, i64, vp, i64,
+                                        i64, f64, vp, i64, i64, i64]),
+    "tcb_dgemv": (i32, [i32, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64]),
+    "tcb_dger": (i32, [i64, i64, f64, vp, i64, vp, i64, vp, i64]),
+    "tcb_ddot": (i32, [i64, vp, i64, vp, i64, P_f64]),
+    "tcb_permute": (i32, [i32, P_i64, P_i64, vp, vp]),
+    "tcb_timer_start": (i32, []),
+    "tcb_timer_stop": (i32, [C.POINTER(C.c_float)]),
+    "tcb_launch_count": (i64, []),
+    "tcb_reset_launch_count": (None, []),
+}
+
+TCF_API = {
+    "tcf_report": (i32, [cp, i32, cp, cp, i64]),
+    "tcf_execute": (i32, [cp, i32, cp, C.c_uint64, i32, i32, i32, cp, cp, vp, i64, P_i64,
+                          P_f64, cp, i64]),
+    "tcf_seeded": (i32, [i64, C.c_uint64, vp]),
+    "tcf_prepare": (i32, [cp, i32, cp, i32, C.POINTER(vp), cp, i64]),
+    "tcf_upload": (i32, [vp, vp, vp]),
+    "tcf_run": (i32, [vp]),
+    "tcf_download": (i32, [vp, vp]),
+    "tcf_sync": (i32, [vp]),
+    "tcf_info": (i32, [vp, P_i64, cp, i64]),
+    "tcf_device_ptrs": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    "tcf_release": (i32, [vp]),
+    "tcf_last_error": (cp, []),
+}
+
+
+def _bind(lib: C.CDLL, api: dict) -> C.CDLL:
+    for name, (res, args) in api.items():
+        fn = getattr(lib, name)  # AttributeError = missing export: fail loudly
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def _ensure_built() -> None:
+    if (LIB / "libtcb200.so").exists() and (LIB / "libtc_b200.so").exists():
+        return
+    from . import build as _build
+    _build.build()
+
+
+def device() -> C.CDLL:
+    """libtcb200.so: the tcb_* device C-ABI."""
+    with _lock:
+        if "dev" not in _libs:
+            _ensure_built()
+            _libs["dev"] = _bind(C.CDLL(str(LIB / "libtcb200.so")), TCB_API)
+        return _libs["dev"]
+
+
+def front() -> C.CDLL:
+    """libtc_b200.so: the tcf_* plan-level C-ABI over the tc:: front."""
+    with _lock:
+        if "front" not in _libs:
+            _ensure_built()
+            _libs["front"] = _bind(C.CDLL(str(LIB / "libtc_b200.so")), TCF_API)
+        return _libs["front"]
+
+
+class TcbError(RuntimeError):
+    pass
+
+
+def check(status: int, what: str = "tcb") -> None:
+    if status != 0:
+        msg = device().tcb_last_error().decode()
+        if status == 1:
+            raise ValueError(f"{what}: {msg}")
+        raise TcbError(f"{what}: status {status}: {msg}")
