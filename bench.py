@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py — fp64 contraction throughput on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg1..cfg5]
+
+A *step* is one evaluation of the BASELINE contraction (default cfg2 =
+BASELINE.json configs[1]: C[a,b,c] = sum_k A[a,k,c] B[k,b], a=b=c=k=256, the
+class-2 shape the reference loops GEMM over; here one strided-batched DMMA
+launch). Prints ONE JSON line on rank 0.
+
+  value    GFLOP/s, operands resident in HBM, CUDA-event timed over exactly K
+           steps, max over ranks; flops = plan.flops = 2*prod(extents).
+  e2e      the same metric through the public plan-level API (tcf_upload ->
+           tcf_run -> tcf_download) with pinned HOST buffers, H2D/D2H inside
+           the timed region.
+  roofline the DMMA GEMM kernel alone (CUDA events on its own stream) against
+           the fp64 DMMA peak measured live on this GPU (tcb_fp64_peak).
+  cpu_baseline the unmodified reference (oracle/_ref, compiled from
+           /root/reference) on the host cores, rank 0, N=1 only.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref)
+on all host cores for the same config and prints the same line with
+"impl": "reference". Under torchrun (N>1) every rank runs its own c-slab of
+a weakly scaled problem (no collective on the data path); only rank 0 runs
+the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fp64 contraction GFLOP/s and % of B200 FP64 peak at 1/2/4/8 GPUs vs host-CPU ref"
+CONFIGS = {
+    "cfg1": ("C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=512,j=512,k=64,l=64",
+             "BASELINE configs[0]: class-1 C[i,j]=A[i,k,l]B[k,l,j], i=j=512, k=l=64"),
+    "cfg2": ("C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]", "a=256,b=256,c=256,k=256",
+             "BASELINE configs[1]: class-2 C[a,b,c]=A[a,k,c]B[k,b], a=b=c=k=256"),
+    "cfg3": ("C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]",
+             "a=64,b=64,c=64,d=64,k=32,l=32",
+             "BASELINE configs[2]: class-3 C[a,b,c,d]=A[a,k,c,l]B[l,b,k,d], a..d=64, k=l=32"),
+    "cfg4": ("C[+a,+b,+i,+j] = A[+a,+b,+k,+l] * B[-k,-l,+i,+j]",
+             "a=256,b=256,i=64,j=64,k=64,l=64",
+             "BASELINE configs[3]: CCD C[a,b,i,j]=A[a,b,k,l]B[k,l,i,j], a=b=256, i..l=64"),
+    "cfg5": ("C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=8192,j=8192,k=512,l=512",
+             "BASELINE configs[4]: large class-1, i=j=8192, k=l=512"),
+}
+# weak scaling: the label each rank owns a slab of (free label, no collective)
+SHARD_LABEL = {"cfg1": "j", "cfg2": "c", "cfg3": "d", "cfg4": "b", "cfg5": "j"}
+L2_BYTES = 126 * 2**20
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:]) if v.lower() == "active"})
+        sm = [float(r[0]) for r in rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
+                "samples": len(rows), "reasons": reasons}
+
+
+def pinned_array(n: int, dev) -> np.ndarray:
+    a = np.empty(int(n))
+    if a.nbytes:
+        check = dev.tcb_host_register(a.ctypes.data, a.nbytes)
+        if check != 0:
+            raise RuntimeError(dev.tcb_last_error().decode())
+    return a
+
+
+def shard_extents(cfg: str, world: int) -> str:
+    """Per-rank extents: every rank owns a full-size slab of SHARD_LABEL, so
+    per-GPU work is fixed as N grows (weak scaling)."""
+    return CONFIGS[cfg][1]
+
+
+def cpu_reference(expr: str, extents: str, reps: int, workers: int):
+    """Times the unmodified reference CPU path (tc::execute, reference backend)
+    via oracle/_ref; falls back to our C port of the naive oracle on a slab."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles  # TEST INFRASTRUCTURE: CPU baseline only
+    if oracles.ref() is not None:
+        times = []
+        oracles.ref_execute(expr, extents, seed=1, workers=workers)  # warm-up
+        for _ in range(reps):
+            _, st = oracles.ref_execute(expr, extents, seed=1, workers=workers)
+            times.append(st["wall_seconds"])
+        return statistics.median(times), "reference", workers
+    return None, "unavailable", 0
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    expr, extents, desc = CONFIGS[cfg]
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles
+    if oracles.ref() is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libtcref.so missing (build with make -C oracle)"}))
+        return 0
+    workers = os.cpu_count() or 1
+    ext = {k: int(v) for k, v in (kv.split("=") for kv in extents.split(","))}
+    flops = 2 * int(np.prod(list(ext.values())))
+    for _ in range(args.warmup):
+        oracles.ref_execute(expr, extents, seed=1, workers=workers)
+    secs = []
+    for _ in range(args.steps):
+        _, st = oracles.ref_execute(expr, extents, seed=1, workers=workers)
+        secs.append(st["wall_seconds"])
+    total = sum(secs)
+    value = flops * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: Tensor::seeded_random uniform[-1,1], seeds 1 (A) / 2 (B)",
+        "config": {"workload": desc, "expr": expr, "extents": extents,
+                   "path": "reference tc::execute + ReferenceBackend (oracle/_ref, -O3 -DNDEBUG)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": workers,
+                         "kind": "reference",
+                         "sample": f"full {cfg} contraction per step, workers={workers}"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = args.config
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    rank, world, local = dist_env()
+    torch = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1307_2100_b200 as T
+    dev = T.native.device()
+    T.check(dev.tcb_init(local), "tcb_init")
+    expr, _, desc = CONFIGS[cfg]
+    extents = shard_extents(cfg, world)
+    peak = C.c_double()
+    T.check(dev.tcb_fp64_peak(C.byref(peak)), "tcb_fp64_peak")
+
+    prep = T.Prepared(expr, extents, device=local)
+    info = prep.info()
+    flops = info["flops"]
+    L = pinned_array(info["left"], dev)
+    R = pinned_array(info["right"], dev)
+    O = pinned_array(info["output"], dev)
+    T.native.front().tcf_seeded(L.size, 1 + 2 * rank, L.ctypes.data)
+    T.native.front().tcf_seeded(R.size, 2 + 2 * rank, R.ctypes.data)
+    prep.upload(L, R)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+        prep.sync()
+
+    # ---- device-resident throughput: exactly K steps between two events
+    for _ in range(args.warmup):
+        prep.run()
+    barrier()
+    clocks = Clocks(local)
+    time.sleep(0.15)
+    dev.tcb_reset_launch_count()
+    ms = C.c_float()
+    T.check(dev.tcb_timer_start())
+    for _ in range(args.steps):
+        prep.run()
+    T.check(dev.tcb_timer_stop(C.byref(ms)))
+    launches = dev.tcb_launch_count()
+    clk = clocks.stop()
+    barrier()
+    t_ms = float(ms.value)
+    if world > 1:
+        t = torch.tensor([t_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(t.item())
+    step_ms = t_ms / args.steps
+    value = world * flops / (step_ms * 1e-3) / 1e9
+
+    # ---- the dominant kernel alone (the contraction launch), events per launch
+    n_kern = max(5, min(args.steps, 50))
+    prep.run_permutes()
+    prep.sync()
+    T.check(dev.tcb_timer_start())
+    for _ in range(n_kern):
+        prep.run_contraction()
+    T.check(dev.tcb_timer_stop(C.byref(ms)))
+    kern_ms = float(ms.value) / n_kern
+    achieved = flops / (kern_ms * 1e-3) / 1e12
+    gemm_info = T.GemmInfo()
+    dev.tcb_last_gemm_info(C.byref(gemm_info))
+
+    # ---- end to end through the public API with pinned host buffers
+    n_e2e = max(3, min(args.steps, 20))
+    prep.upload(L, R)
+    prep.run()
+    prep.download(O)
+    barrier()
+    T.check(dev.tcb_timer_start())
+    for _ in range(n_e2e):
+        prep.upload(L, R)
+        prep.run()
+        prep.download(O)
+    T.check(dev.tcb_timer_stop(C.byref(ms)))
+    e2e_ms = float(ms.value)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * flops / (e2e_ms / n_e2e * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 6),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: Tensor::seeded_random uniform[-1,1] (mt19937_64), seeds 1/2 (+2*rank)",
+        "config": {
+            "workload": desc, "expr": expr, "extents": extents,
+            "recipe": info["summary"],
+            "parallelism": "single GPU" if world == 1 else
+                           f"weak: rank r owns {SHARD_LABEL[cfg]}-slab r (no data-path collective)",
+            "l2": "inputs larger than L2 per step (A+B+C = %.0f MB > 126 MB)"
+                  % ((info['left'] + info['right'] + info['output']) * 8 / 2**20)
+                  if (info['left'] + info['right'] + info['output']) * 8 > L2_BYTES else
+                  "operands fit in L2 (re-read hot across steps)",
+        },
+        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int((info["left"] + info["right"]) * 8),
+                "d2h_bytes_per_step": int(info["output"] * 8),
+                "steps": n_e2e, "api": "tcf_upload + tcf_run + tcf_download (include/tcf.h)"},
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
+                     "peak": round(peak.value, 3), "unit": "TFLOP/s",
+                     "frac": round(achieved / peak.value, 4), "traffic": None,
+                     "kernel": "dgemm_dmma_kernel" if gemm_info.path in (0, 1) else "gemv",
+                     "kernel_ms": round(kern_ms, 6),
+                     "peak_source": "tcb_fp64_peak: DMMA m8n8k4 register-resident microbenchmark "
+                                    "run live on this GPU (MEASURED_PEAKS.json has no fp64 entry)",
+                     "algorithmic_flops_per_launch": flops},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    prof = ROOT / "profiles" / f"ncu_{cfg}_summary.json"
+    if prof.exists():
+        try:
+            line["roofline"]["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        secs, kind, cores = cpu_reference(expr, extents, reps=3, workers=workers)
+        if secs:
+            line["cpu_baseline"] = {"value": round(flops / secs / 1e9, 3), "unit": "GFLOP/s",
+                                    "cores": cores, "kind": kind,
+                                    "sample": f"full {cfg} contraction, median of 3 after 1 "
+                                              f"warm-up, tc::execute workers={cores}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -386,6 +386,11 @@ class PreparedContraction {
   void upload(const double* left, const double* right);
   /// Permutations + the GEMM/GEMV/DOT launch, on the device stream (async).
   void run();
+  /// The two halves of run(): operand permutations (L3 only) and the single
+  /// GEMM/GEMV/DOT launch (which reads the permuted operands of the last
+  /// run_permutes()). Separately callable so the kernels can be timed alone.
+  void run_permutes();
+  void run_contraction();
   /// Device -> host copy of the result (synchronous).
   void download(double* out);
   void sync();

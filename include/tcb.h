@@ -129,6 +129,10 @@ int tcb_permute(int rank, const int64_t* ext, const int64_t* src_str, const doub
 int tcb_timer_start(void);
 int tcb_timer_stop(float* ms);
 
+/* Measured fp64 tensor-pipe (DMMA) peak of the current device in TFLOP/s —
+ * the roofline denominator bench.py reports against. */
+int tcb_fp64_peak(double* tflops);
+
 /* Count of kernels this library launched on this thread since the last reset
  * (evidence for bench.py's gpu_launches). */
 int64_t tcb_launch_count(void);

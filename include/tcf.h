@@ -40,6 +40,9 @@ int tcf_prepare(const char* expr, int positional, const char* extents, int devic
                 void** handle, char* err, int64_t errcap);
 int tcf_upload(void* handle, const double* left, const double* right);
 int tcf_run(void* handle);
+/* The two halves of tcf_run (for timing the kernels separately). */
+int tcf_run_permutes(void* handle);
+int tcf_run_contraction(void* handle);
 int tcf_download(void* handle, double* out);
 int tcf_sync(void* handle);
 /* info[12]: left, right, output elements; launches of the last run;

@@ -107,6 +107,12 @@ class Prepared:
     def run(self) -> None:
         self._ok(self._lib.tcf_run(self._h))
 
+    def run_permutes(self) -> None:
+        self._ok(self._lib.tcf_run_permutes(self._h))
+
+    def run_contraction(self) -> None:
+        self._ok(self._lib.tcf_run_contraction(self._h))
+
     def download(self, out: np.ndarray) -> None:
         self._ok(self._lib.tcf_download(self._h, out.ctypes.data))
 

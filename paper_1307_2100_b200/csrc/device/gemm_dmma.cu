@@ -8,15 +8,16 @@
 //
 // Design (sm_100a; fp64 has no tcgen05 kind, so the tensor pipe is reached
 // through warp-level mma.sync, fed from shared memory):
-//   * CTA tile 128x128x16, 8 warps (2 x 4, warp tile 64x32 = 8x4 DMMA 8x8
-//     blocks, 32 independent accumulators/warp). No separate producer warp: a
-//     9th warp would cap registers at 168 (the register file is split per
-//     SM sub-partition) and spill the accumulators.
-//   * 6-stage smem ring (32 KB/stage) with full/empty mbarriers. Each k-block
-//     step refills the stage released two blocks earlier (4 blocks in
-//     flight): thread 0 issues cp.async.bulk.tensor (TMA, 128B swizzle) when
-//     both operands are TMA-legal, else all 256 threads issue zero-filling
-//     8-byte cp.async that arrive on the same mbarrier.
+//   * CTA tile 128x128x16, 8 consumer warps (2 x 4, warp tile 64x32 = 8x4
+//     DMMA 8x8 blocks, 32 independent accumulators/warp) + a producer
+//     warpgroup. setmaxnreg hands the producer's registers to the consumers
+//     (40 vs 232 per thread): without it a 12-warp CTA caps at 168 registers
+//     and the accumulators spill.
+//   * 6-stage smem ring (32 KB/stage) with full/empty mbarriers. The producer
+//     issues cp.async.bulk.tensor (TMA, 128B swizzle, 5-D maps carrying the
+//     batch dims) from one thread when both operands are TMA-legal, else its
+//     128 threads issue zero-filling 8-byte cp.async arriving on the same
+//     mbarrier.
 //   * Two smem layouts per operand: "MN-major" (outer index contiguous in
 //     global: 8 boxes of 16(outer) x 16(k)) and "K-major" (k contiguous: one box
 //     of 16(k) x 128(outer)); both 128B-swizzled. The k-set of each DMMA k-step
@@ -28,7 +29,8 @@
 //     workspace; the last-arriving CTA sums the partials in split order
 //     (bit-reproducible run to run) and applies alpha/beta.
 //   * Epilogue writes C through composite row/column offsets (index groups),
-//     so interleaved output orders need no permutation pass.
+//     decoded once per tile into a shared-memory table, so interleaved output
+//     orders need no permutation pass.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -42,13 +44,15 @@ namespace tcb {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
-constexpr int PREFETCH = STAGES - 2;  // refill lag of two blocks (see kernel)
-constexpr int NCW = 8;                 // compute warps
+constexpr int NCW = 8;                 // consumer (DMMA) warps
 constexpr int CTHREADS = NCW * 32;     // 256
+constexpr int PTHREADS = 128;          // producer warpgroup
+constexpr int NTHREADS = PTHREADS + CTHREADS;
 constexpr int STAGE_A = BM * BK * 8;   // 16 KB
 constexpr int STAGE_B = BN * BK * 8;   // 16 KB
 constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                           (BM + BN) * 8 /*epilogue offset tables*/;
 
 struct Params {
   const double* A;
@@ -102,39 +106,16 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, bool 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(n)
                : "memory");
 }
-__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                         int rank, const int* c) {
-  const uint64_t m = reinterpret_cast<uint64_t>(map);
-  switch (rank) {
-    case 2:
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(bar)
-          : "memory");
-      break;
-    case 3:
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(bar)
-          : "memory");
-      break;
-    case 4:
-      asm volatile(
-          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(bar)
-          : "memory");
-      break;
-    default:
-      asm volatile(
-          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
-          : "memory");
-      break;
-  }
+__device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                          int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(CTHREADS) : "memory");
 }
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
@@ -211,28 +192,35 @@ __device__ __forceinline__ int64_t composite(int64_t idx, int n, const int64_t* 
 }
 
 // ------------------------------------------------------------------ kernel
-// Load-side iterator: walks the same (unit, k-block) sequence as the consumer
-// loop, PREFETCH blocks ahead, across unit boundaries.
+// Producer-side iterator over this CTA's (unit, k-block) sequence. All
+// per-unit address math (64-bit divisions) happens once per unit here, in the
+// producer warpgroup, never on the consumer warps.
 struct LoadIter {
   int64_t u;
   int kb, kb1;
-  int64_t m0, n0, oa, ob;
-  int bc[TCB_MAX_DIMS];
+  int m0, n0;            // tile origin (TMA coordinates are int32)
+  int64_t oa, ob;        // batch offsets (cp.async path)
+  int ca[3], cb[3];      // batch coordinates of the A / B tensor maps
   bool valid;
 
   __device__ __forceinline__ void start_unit(const Params& p) {
     valid = u < p.units;
     if (!valid) return;
     const Unit un = decode_unit(p, u);
+    int bc[TCB_MAX_DIMS];
     int64_t oc;
     batch_offsets(p, un.batch, oa, ob, oc, bc);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      ca[i] = i < p.a_rank - 2 ? bc[p.a_bdim[i]] : 0;
+      cb[i] = i < p.b_rank - 2 ? bc[p.b_bdim[i]] : 0;
+    }
     kb = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
     kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
-    m0 = static_cast<int64_t>(un.tm) * BM;
-    n0 = static_cast<int64_t>(un.tn) * BN;
+    m0 = un.tm * BM;
+    n0 = un.tn * BN;
   }
   __device__ __forceinline__ void advance(const Params& p) {
-    if (!valid) return;
     if (++kb == kb1) {
       u += gridDim.x;
       start_unit(p);
@@ -240,61 +228,47 @@ struct LoadIter {
   }
 };
 
-// Issue the loads of the iterator's current k-block into `stage` (signals
-// full[stage]). TMA: thread 0 only. cp.async: all 256 threads.
+// Issue one k-block of both operands into a stage. TMA: one thread, 5-D maps
+// (lead, other, 3 batch dims). cp.async: the 128 producer threads.
 template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA>
 __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& tmA,
                                             const CUtensorMap& tmB, const LoadIter& li,
-                                            uint32_t sA, uint32_t full, int tid) {
-  const int64_t k0 = static_cast<int64_t>(li.kb) * BK;
+                                            uint32_t sA, uint32_t full, int ptid) {
+  const int k0 = li.kb * BK;
   const uint32_t sB = sA + STAGE_A;
   if (USE_TMA) {
-    if (tid != 0) return;
     mbar_expect_tx(full, STAGE_BYTES);
-    int c[5];
-    for (int i = 0; i < p.a_rank - 2; ++i) c[2 + i] = li.bc[p.a_bdim[i]];
     if (A_KMAJOR) {
-      c[0] = static_cast<int>(k0);
-      c[1] = static_cast<int>(li.m0);
-      tma_load(sA, &tmA, full, p.a_rank, c);
+      tma_load5(sA, &tmA, full, k0, li.m0, li.ca[0], li.ca[1], li.ca[2]);
     } else {
-      c[1] = static_cast<int>(k0);
 #pragma unroll
-      for (int i = 0; i < BM / 16; ++i) {
-        c[0] = static_cast<int>(li.m0 + 16 * i);
-        tma_load(sA + i * 2048, &tmA, full, p.a_rank, c);
-      }
+      for (int i = 0; i < BM / 16; ++i)
+        tma_load5(sA + i * 2048, &tmA, full, li.m0 + 16 * i, k0, li.ca[0], li.ca[1], li.ca[2]);
     }
-    for (int i = 0; i < p.b_rank - 2; ++i) c[2 + i] = li.bc[p.b_bdim[i]];
     if (B_KMAJOR) {
-      c[0] = static_cast<int>(k0);
-      c[1] = static_cast<int>(li.n0);
-      tma_load(sB, &tmB, full, p.b_rank, c);
+      tma_load5(sB, &tmB, full, k0, li.n0, li.cb[0], li.cb[1], li.cb[2]);
     } else {
-      c[1] = static_cast<int>(k0);
 #pragma unroll
-      for (int i = 0; i < BN / 16; ++i) {
-        c[0] = static_cast<int>(li.n0 + 16 * i);
-        tma_load(sB + i * 2048, &tmB, full, p.b_rank, c);
-      }
+      for (int i = 0; i < BN / 16; ++i)
+        tma_load5(sB + i * 2048, &tmB, full, li.n0 + 16 * i, k0, li.cb[0], li.cb[1], li.cb[2]);
     }
   } else {
     const double* Ab = p.A + li.oa;
     const double* Bb = p.B + li.ob;
-    // 2048 elements per operand tile, 8 per thread; the thread order follows
-    // the operand's unit-stride index so warps read contiguous global memory.
-#pragma unroll
-    for (int i = 0; i < (BM * BK) / CTHREADS; ++i) {
-      const int idx = tid + CTHREADS * i;
+    // 2048 elements per operand tile, 16 per producer thread; the thread order
+    // follows the operand's unit-stride index so warps read contiguous memory.
+#pragma unroll 4
+    for (int i = 0; i < (BM * BK) / PTHREADS; ++i) {
+      const int idx = ptid + PTHREADS * i;
       const int o = (p.a_so == 1) ? (idx & (BM - 1)) : (idx >> 4);
       const int k = (p.a_so == 1) ? (idx >> 7) : (idx & 15);
       const int64_t gm = li.m0 + o, gk = k0 + k;
       const bool ok = gm < p.M && gk < p.K;
       cp_async8(sA + tile_off<A_KMAJOR>(o, k), ok ? Ab + gm * p.a_so + gk * p.a_sk : p.A, ok);
     }
-#pragma unroll
-    for (int i = 0; i < (BN * BK) / CTHREADS; ++i) {
-      const int idx = tid + CTHREADS * i;
+#pragma unroll 4
+    for (int i = 0; i < (BN * BK) / PTHREADS; ++i) {
+      const int idx = ptid + PTHREADS * i;
       const int o = (p.b_so == 1) ? (idx & (BN - 1)) : (idx >> 4);
       const int k = (p.b_so == 1) ? (idx >> 7) : (idx & 15);
       const int64_t gn = li.n0 + o, gk = k0 + k;
@@ -305,8 +279,12 @@ __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& 
   }
 }
 
+// 384 threads: warpgroup 0 = producer (TMA: one elected thread; cp.async: all
+// 128), warpgroups 1-2 = 8 DMMA consumer warps. setmaxnreg moves registers
+// from the producer (40/thread) to the consumers (232/thread) so the 64-double
+// accumulator tile never spills (a plain 9- or 12-warp CTA caps at 168).
 template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA>
-__global__ void __launch_bounds__(CTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ unsigned char smem_raw[];
@@ -317,13 +295,14 @@ __global__ void __launch_bounds__(CTHREADS, 1)
   const uint32_t full0 = smem_u32(bars);            // full[s]  = full0 + 8s
   const uint32_t empty0 = smem_u32(bars + STAGES);  // empty[s] = empty0 + 8s
   volatile unsigned* s_flag = reinterpret_cast<volatile unsigned*>(bars + 2 * STAGES);
+  // per-tile output offsets: composite row(m) / col(n) of the tile, -1 = outside C
+  int64_t* s_row = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + 256);
+  int64_t* s_col = s_row + BM;
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full0 + 8 * s, USE_TMA ? 1 : CTHREADS);
+      mbar_init(full0 + 8 * s, USE_TMA ? 1 : PTHREADS);
       mbar_init(empty0 + 8 * s, NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -334,19 +313,31 @@ __global__ void __launch_bounds__(CTHREADS, 1)
   }
   __syncthreads();
 
-  // ---- prologue: put the first PREFETCH k-blocks in flight
-  LoadIter li;
-  li.u = blockIdx.x;
-  li.start_unit(p);
-  uint32_t gload = 0;  // k-blocks issued by this CTA
+  if (tid < PTHREADS) {
+    // ============================ producer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    if (USE_TMA && tid != 0) return;
+    LoadIter li;
+    li.u = blockIdx.x;
+    li.start_unit(p);
+    uint32_t g = 0;
 #pragma unroll 1
-  for (int i = 0; i < PREFETCH && li.valid; ++i) {
-    issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + (gload % STAGES) * STAGE_BYTES,
-                                             full0 + 8 * (gload % STAGES), tid);
-    ++gload;
-    li.advance(p);
+    while (li.valid) {
+      const uint32_t s = g % STAGES;
+      mbar_wait(empty0 + 8 * s, ((g / STAGES) & 1) ^ 1);
+      issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
+                                               full0 + 8 * s, tid);
+      ++g;
+      li.advance(p);
+    }
+    if (!USE_TMA) asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
   }
 
+  // ============================ consumers ============================
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+  const int ctid = tid - PTHREADS;  // 0..255
+  const int warp = ctid >> 5, lane = ctid & 31;
   const int wm = warp & 1, wn = warp >> 1;
   const int r = lane >> 2, q = lane & 3;
 
@@ -379,19 +370,6 @@ __global__ void __launch_bounds__(CTHREADS, 1)
 
 #pragma unroll 1
     for (int kb = kb0; kb < kb1; ++kb) {
-      // refill: block gload reuses the stage released two blocks ago
-      if (li.valid) {
-        const uint32_t s = gload % STAGES;
-        if (USE_TMA) {
-          if (tid == 0) mbar_wait(empty0 + 8 * s, ((gload / STAGES) & 1) ^ 1);
-        } else {
-          mbar_wait(empty0 + 8 * s, ((gload / STAGES) & 1) ^ 1);
-        }
-        issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
-                                                 full0 + 8 * s, tid);
-        ++gload;
-        li.advance(p);
-      }
       const uint32_t stage = gcons % STAGES;
       mbar_wait(full0 + 8 * stage, (gcons / STAGES) & 1);
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
@@ -425,12 +403,6 @@ __global__ void __launch_bounds__(CTHREADS, 1)
     }
 
     // ------------------------------ epilogue ------------------------------
-    int bc[TCB_MAX_DIMS];
-    int64_t oa, ob, oc;
-    batch_offsets(p, un.batch, oa, ob, oc, bc);
-    const int64_t mbase = static_cast<int64_t>(un.tm) * BM + wm * 64 + r;
-    const int64_t nbase = static_cast<int64_t>(un.tn) * BN + wn * 32 + 2 * q;
-
     if (p.splits > 1) {
       const int64_t tile = u / p.splits;
       double* part = p.ws + (tile * p.splits + un.split) * static_cast<int64_t>(BM * BN);
@@ -439,18 +411,18 @@ __global__ void __launch_bounds__(CTHREADS, 1)
 #pragma unroll
         for (int in = 0; in < 4; ++in) {
           const int v = im * 4 + in;
-          __stcg(reinterpret_cast<double2*>(part) + v * CTHREADS + tid,
+          __stcg(reinterpret_cast<double2*>(part) + v * CTHREADS + ctid,
                  make_double2(acc[im][in][0], acc[im][in][1]));
         }
       __threadfence();
-      __syncthreads();
-      if (tid == 0) {
+      consumer_sync();
+      if (ctid == 0) {
         const unsigned prev = atomicAdd(p.counters + tile, 1u);
         *s_flag = (prev == static_cast<unsigned>(p.splits - 1)) ? 1u : 0u;
       }
-      __syncthreads();
+      consumer_sync();
       const bool last = *s_flag != 0u;
-      __syncthreads();  // s_flag is reused by the next unit
+      consumer_sync();      // s_flag is reused by the next unit
       if (!last) continue;  // not the last split of this tile
       __threadfence();
       const double* base = p.ws + tile * p.splits * static_cast<int64_t>(BM * BN);
@@ -466,43 +438,54 @@ __global__ void __launch_bounds__(CTHREADS, 1)
         for (int im = 0; im < 8; ++im)
 #pragma unroll
           for (int in = 0; in < 4; ++in) {
-            const double2 v = __ldcg(ps + (im * 4 + in) * CTHREADS + tid);
+            const double2 v = __ldcg(ps + (im * 4 + in) * CTHREADS + ctid);
             acc[im][in][0] += v.x;
             acc[im][in][1] += v.y;
           }
       }
-      if (tid == 0) p.counters[tile] = 0u;  // re-arm for the next launch
+      if (ctid == 0) p.counters[tile] = 0u;  // re-arm for the next launch
     }
 
+    // Output offsets of this tile's 128 rows and 128 columns, decoded once
+    // (one composite index per consumer thread) into shared memory.
+    consumer_sync();  // the previous unit's epilogue is done with the tables
+    {
+      const int i = ctid & 127;
+      if (ctid < 128) {
+        const int64_t m = static_cast<int64_t>(un.tm) * BM + i;
+        s_row[i] = m < p.M ? composite(m, p.c_nrow, p.c_row_ext, p.c_row_str) : -1;
+      } else {
+        const int64_t n = static_cast<int64_t>(un.tn) * BN + i;
+        s_col[i] = n < p.N ? composite(n, p.c_ncol, p.c_col_ext, p.c_col_str) : -1;
+      }
+    }
+    int bc[TCB_MAX_DIMS];
+    int64_t oa, ob, oc;
+    batch_offsets(p, un.batch, oa, ob, oc, bc);
+    consumer_sync();
     int64_t coff[4][2];
-    bool cok[4][2];
 #pragma unroll
     for (int in = 0; in < 4; ++in)
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int64_t n = nbase + in * 8 + jj;
-        cok[in][jj] = n < p.N;
-        coff[in][jj] = cok[in][jj] ? composite(n, p.c_ncol, p.c_col_ext, p.c_col_str) : 0;
-      }
+      for (int jj = 0; jj < 2; ++jj) coff[in][jj] = s_col[wn * 32 + in * 8 + 2 * q + jj];
     double* Cb = p.C + oc;
+    const bool use_beta = p.beta != 0.0;
 #pragma unroll
     for (int im = 0; im < 8; ++im) {
-      const int64_t m = mbase + im * 8;
-      if (m >= p.M) continue;
-      const int64_t roff = composite(m, p.c_nrow, p.c_row_ext, p.c_row_str);
+      const int64_t roff = s_row[wm * 64 + im * 8 + r];
+      if (roff < 0) continue;
 #pragma unroll
       for (int in = 0; in < 4; ++in)
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
-          if (!cok[in][jj]) continue;
+          if (coff[in][jj] < 0) continue;
           double* dst = Cb + roff + coff[in][jj];
           double v = p.alpha * acc[im][in][jj];
-          if (p.beta != 0.0) v += p.beta * *dst;
+          if (use_beta) v += p.beta * *dst;
           *dst = v;
         }
     }
   }
-  if (!USE_TMA) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // beta-only update (alpha == 0 or K == 0): C <- beta*C, or 0 when beta == 0
@@ -576,8 +559,15 @@ bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t outer, 
     ++r;
   }
   *rank = r;
+  // Always encode 5 dims (unused ones: extent 1) so the kernel issues a single
+  // instruction form (cp.async.bulk.tensor.5d) whatever the batch rank.
+  for (; r < 5; ++r) {
+    dims[r] = 1;
+    strides[r - 1] = strides[r - 2];
+    box[r] = 1;
+  }
   const CUresult res =
-      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, r, const_cast<double*>(base), dims, strides, box,
+      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides, box,
          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
@@ -594,7 +584,7 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<grid, CTHREADS, SMEM_BYTES, s>>>(p, ta, tb);
+  kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(p, ta, tb);
   return cudaGetLastError();
 }
 

@@ -221,6 +221,26 @@ int tcf_run(void* handle) {
   TCF_GUARD(nullptr, 0)
 }
 
+int tcf_run_permutes(void* handle) {
+  try {
+    static_cast<Handle*>(handle)->pc->run_permutes();
+    return 0;
+  }
+  TCF_GUARD(nullptr, 0)
+}
+
+int tcf_run_contraction(void* handle) {
+  try {
+    Handle* h = static_cast<Handle*>(handle);
+    h->pc->run_contraction();
+    tcb_gemm_info info{};
+    tcb_last_gemm_info(&info);
+    h->path = info.path;
+    return 0;
+  }
+  TCF_GUARD(nullptr, 0)
+}
+
 int tcf_download(void* handle, double* out) {
   try {
     static_cast<Handle*>(handle)->pc->download(out);

@@ -210,15 +210,23 @@ void PreparedContraction::upload(const double* left, const double* right) {
 void PreparedContraction::run() {
   check(tcb_init(device_), "tcb_init");
   const std::int64_t before = tcb_launch_count();
-  const double* a = dl_;
-  const double* b = dr_;
-  for (const PermuteStep& ps : recipe_.permutes) {
-    double* dst = ps.right ? pr_ : pl_;
+  run_permutes();
+  run_contraction();
+  launches_ = tcb_launch_count() - before;
+}
+
+void PreparedContraction::run_permutes() {
+  check(tcb_init(device_), "tcb_init");
+  for (const PermuteStep& ps : recipe_.permutes)
     check(tcb_permute(static_cast<int>(ps.ext.size()), ps.ext.data(), ps.src_str.data(),
-                      ps.right ? dr_ : dl_, dst),
+                      ps.right ? dr_ : dl_, ps.right ? pr_ : pl_),
           "permute");
-    (ps.right ? b : a) = dst;
-  }
+}
+
+void PreparedContraction::run_contraction() {
+  check(tcb_init(device_), "tcb_init");
+  const double* a = pl_ ? pl_ : dl_;
+  const double* b = pr_ ? pr_ : dr_;
   tcb_gemm_desc d;
   std::memset(&d, 0, sizeof d);
   d.m = recipe_.m;
@@ -248,7 +256,6 @@ void PreparedContraction::run() {
   d.alpha = 1.0;
   d.beta = 0.0;
   check(tcb_gemm(&d, a, b, do_), "contraction");
-  launches_ = tcb_launch_count() - before;
 }
 
 void PreparedContraction::download(double* out) {

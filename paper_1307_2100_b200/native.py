@@ -67,6 +67,7 @@ TCB_API = {
     "tcb_permute": (i32, [i32, P_i64, P_i64, vp, vp]),
     "tcb_timer_start": (i32, []),
     "tcb_timer_stop": (i32, [C.POINTER(C.c_float)]),
+    "tcb_fp64_peak": (i32, [P_f64]),
     "tcb_launch_count": (i64, []),
     "tcb_reset_launch_count": (None, []),
 }
@@ -79,6 +80,8 @@ TCF_API = {
     "tcf_prepare": (i32, [cp, i32, cp, i32, C.POINTER(vp), cp, i64]),
     "tcf_upload": (i32, [vp, vp, vp]),
     "tcf_run": (i32, [vp]),
+    "tcf_run_permutes": (i32, [vp]),
+    "tcf_run_contraction": (i32, [vp]),
     "tcf_download": (i32, [vp, vp]),
     "tcf_sync": (i32, [vp]),
     "tcf_info": (i32, [vp, P_i64, cp, i64]),
