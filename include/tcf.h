@@ -32,6 +32,10 @@ int tcf_execute(const char* expr, int positional, const char* extents, uint64_t 
                 double* out, int64_t out_cap, int64_t* stats, double* seconds, char* err,
                 int64_t errcap);
 
+/* The device recipe (lowering) of a contraction, without touching a device:
+ * "L1|L2|L3 gemm m=.. n=.. k=.. a(sm,sk) b(sk,sn) batch=[..] permutes=N". */
+int tcf_lower(const char* expr, int positional, const char* extents, char* buf, int64_t cap);
+
 /* Fill `out` with Tensor::seeded_random's stream (src/tensor.cpp:54-62). */
 int tcf_seeded(int64_t n, uint64_t seed, double* out);
 

@@ -20,7 +20,7 @@ from .native import GemmDesc, GemmInfo, TcbError, check
 
 KERNELS = ["GEMM", "COPY+GEMM", "GEMV", "COPY+GEMV", "GER", "DOT", "ELEMENTWISE"]
 
-__all__ = ["report", "execute", "seeded", "Prepared", "DeviceBuffer", "GemmDesc", "GemmInfo",
+__all__ = ["report", "lower", "execute", "seeded", "Prepared", "DeviceBuffer", "GemmDesc", "GemmInfo",
            "TcbError", "check", "native", "KERNELS", "parse_expr"]
 
 
@@ -39,6 +39,14 @@ def report(expr: str, extents: str, positional: bool = False) -> str:
     """Deterministic analysis text (class, slicing catalogue, plans)."""
     buf = C.create_string_buffer(1 << 20)
     rc = native.front().tcf_report(expr.encode(), int(positional), extents.encode(), buf, len(buf))
+    _err(rc, buf)
+    return buf.value.decode()
+
+
+def lower(expr: str, extents: str, positional: bool = False) -> str:
+    """The device recipe chosen for a contraction (no device needed)."""
+    buf = C.create_string_buffer(4096)
+    rc = native.front().tcf_lower(expr.encode(), int(positional), extents.encode(), buf, len(buf))
     _err(rc, buf)
     return buf.value.decode()
 

@@ -179,6 +179,18 @@ int tcf_execute(const char* expr, int positional, const char* extents, uint64_t 
   TCF_GUARD(err, errcap)
 }
 
+int tcf_lower(const char* expr, int positional, const char* extents, char* buf, int64_t cap) {
+  try {
+    const tc::ContractionSpec spec = tc::parse(expr ? expr : "", positional != 0);
+    const Shapes s = shapes_of(spec, parse_extents(extents));
+    const std::string text = tc::lower(tc::validate_shapes(spec, s.le, s.lv, s.re, s.rv)).summary();
+    if (static_cast<std::int64_t>(text.size()) + 1 > cap) return 4;
+    std::memcpy(buf, text.c_str(), text.size() + 1);
+    return 0;
+  }
+  TCF_GUARD(buf, cap)
+}
+
 int tcf_seeded(int64_t n, uint64_t seed, double* out) {
   std::mt19937_64 gen(seed);
   std::uniform_real_distribution<double> u(-1.0, 1.0);

@@ -1,0 +1,163 @@
+// Executor and backend suites restated from the reference's doctest files
+// (tests/test_executor.cpp, tests/test_kernels.cpp) against the engine's
+// device path: tc::execute with make_backend("b200"). Requires a B200.
+#include <random>
+
+#include "harness.hpp"
+#include "helpers.hpp"
+
+using namespace tc;
+using tst::bind_expr;
+
+namespace {
+const auto kBackend = make_backend("b200");
+
+// direct nested summation (src/oracle.cpp:32-94 order) for small cases
+Tensor naive(const ValidatedContraction& v, const Tensor& L, const Tensor& R) {
+  Tensor out(v.output_extents(), v.output_variance());
+  std::vector<int> fr;
+  for (const auto& ix : v.spec.output.indices) fr.push_back(v.label_index(ix.label));
+  std::vector<std::int64_t> fc(fr.size(), 0);
+  auto lstr = [&](int li) {
+    const auto& i = v.labels[li];
+    return i.left_mode >= 0 ? stride_of(L, i.left_mode) : 0;
+  };
+  auto rstr = [&](int li) {
+    const auto& i = v.labels[li];
+    return i.right_mode >= 0 ? stride_of(R, i.right_mode) : 0;
+  };
+  for (std::int64_t o = 0; o < out.size(); ++o) {
+    std::int64_t t = o, lb = 0, rb = 0;
+    for (std::size_t i = 0; i < fr.size(); ++i) {
+      const std::int64_t e = v.labels[fr[i]].extent, c = t % e;
+      t /= e;
+      lb += c * lstr(fr[i]);
+      rb += c * rstr(fr[i]);
+    }
+    std::int64_t total = 1;
+    for (int ci : v.contracted) total *= v.labels[ci].extent;
+    double acc = 0;
+    for (std::int64_t q = 0; q < total; ++q) {
+      std::int64_t u = q, lo = lb, ro = rb;
+      for (int ci : v.contracted) {
+        const std::int64_t e = v.labels[ci].extent, c = u % e;
+        u /= e;
+        lo += c * lstr(ci);
+        ro += c * rstr(ci);
+      }
+      acc += L.data()[lo] * R.data()[ro];
+    }
+    out.data()[o] = acc;
+  }
+  return out;
+}
+}  // namespace
+
+TEST_CASE("plain matrix product runs as a single device launch") {  // test_executor.cpp:20-30
+  const auto b = bind_expr("C[+i,-j] = A[+i,+h] * B[-h,-j]", {{"i", 2}, {"j", 2}, {"h", 2}});
+  const auto p = plan(b.v);
+  auto [result, stats] = execute(p, b.v, b.left, b.right, *kBackend);
+  CHECK(stats.kernel_calls == 1);
+  CHECK(stats.packed_bytes == 0);
+  CHECK(stats.flops == p.flops);
+  CHECK(max_rel_error(result, naive(b.v, b.left, b.right)) <= 1e-15);
+}
+
+TEST_CASE("crossed stride-1 contraction permutes and matches the oracle") {
+  const auto b = bind_expr("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]",
+                           {{"a", 4}, {"b", 4}, {"g", 4}, {"e", 4}});
+  const auto p = plan(b.v);
+  REQUIRE(p.kernel == KernelKind::CopyGemm);
+  auto [result, stats] = execute(p, b.v, b.left, b.right, *kBackend);
+  CHECK(stats.packed_bytes > 0);
+  CHECK(max_rel_error(result, naive(b.v, b.left, b.right)) <= 1e-12);
+}
+
+TEST_CASE("full contraction to a scalar") {  // test_executor.cpp:43-54
+  const auto b = bind_expr("K[] = T[+a,+b,+g] * S[-a,-b,-g]", {{"a", 3}, {"b", 3}, {"g", 3}});
+  auto [result, stats] = execute(plan(b.v), b.v, b.left, b.right, *kBackend);
+  double expect = 0;
+  for (std::int64_t i = 0; i < b.left.size(); ++i) expect += b.left.data()[i] * b.right.data()[i];
+  CHECK(std::abs(result.at({}) - expect) <= 1e-13 * std::abs(expect) + 1e-15);
+}
+
+TEST_CASE("auto plans match the oracle across a randomized family") {
+  std::mt19937_64 rng(31337);
+  const char* exprs[] = {"R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]",
+                         "R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]",
+                         "R[+a,+b,+c,+d] = X[+i,+a,+j,+b] * Y[-j,+c,-i,+d]",
+                         "R[+g] = T[+a,+b,+g] * G[-a,-b]"};
+  for (int it = 0; it < 40; ++it) {
+    std::map<std::string, std::int64_t> ext;
+    for (const char* l : {"a", "b", "c", "d", "e", "g", "i", "j"})
+      ext[l] = 1 + static_cast<std::int64_t>(rng() % 6);
+    const auto b = bind_expr(exprs[it % 4], ext, it);
+    auto [r, s] = execute(plan(b.v), b.v, b.left, b.right, *kBackend);
+    CHECK(max_rel_error(r, naive(b.v, b.left, b.right)) <= 1e-12);
+  }
+}
+
+TEST_CASE("every enumerated slicing computes the same tensor") {  // test_executor.cpp:89-102
+  const auto b = bind_expr("C[+i,-j] = A[+i,+h] * B[-h,-j]", {{"i", 3}, {"j", 3}, {"h", 3}});
+  const auto runs = execute_all_slicings(b.v, b.left, b.right, *kBackend);
+  REQUIRE(!runs.empty());
+  for (const auto& r : runs) CHECK(max_rel_error(r.result, runs[0].result) <= 1e-12);
+  CHECK_THROWS_AS(execute_all_slicings(b.v, b.left, b.right, *kBackend, 10), resource_limit_error);
+}
+
+TEST_CASE("worker count does not change the result") {  // test_executor.cpp:209-219
+  const auto b = bind_expr("R[+a,+b,+c,+d] = X[+i,+a,+j,+b] * Y[-i,+c,-j,+d]",
+                           {{"a", 3}, {"b", 4}, {"c", 3}, {"d", 4}, {"i", 3}, {"j", 3}});
+  const auto p = plan(b.v);
+  auto [r1, s1] = execute(p, b.v, b.left, b.right, *kBackend, 1);
+  auto [r2, s2] = execute(p, b.v, b.left, b.right, *kBackend, 3);
+  CHECK(tensor_hash(r1) == tensor_hash(r2));
+}
+
+TEST_CASE("extent drift between planning and execution is rejected") {  // :221-229
+  const auto b = bind_expr("C[+i,-j] = A[+i,+h] * B[-h,-j]", {{"i", 3}, {"j", 3}, {"h", 3}});
+  const auto p = plan(b.v);
+  const auto b2 = bind_expr("C[+i,-j] = A[+i,+h] * B[-h,-j]", {{"i", 4}, {"j", 4}, {"h", 4}});
+  CHECK_THROWS_AS(execute(p, b2.v, b2.left, b2.right, *kBackend), std::invalid_argument);
+}
+
+TEST_CASE("device faults surface with the contraction attached") {  // :240-291
+  const auto b = bind_expr("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]",
+                           {{"a", 3}, {"b", 3}, {"g", 3}, {"e", 3}});
+  B200Options o;
+  o.fail_after_launches = 0;
+  const auto failing = make_b200_backend(o);
+  try {
+    execute(plan(b.v), b.v, b.left, b.right, *failing);
+    CHECK(false);
+  } catch (const std::runtime_error& e) {
+    const std::string what = e.what();
+    CHECK(what.find("synthetic device fault") != std::string::npos);
+    CHECK(what.find("R[+a,-e]") != std::string::npos);
+  }
+}
+
+TEST_CASE("backend gemm/gemv/ger/dot known answers on host pointers") {  // test_kernels.cpp
+  const std::vector<double> A{1, 3, 2, 4}, B{5, 7, 6, 8};
+  std::vector<double> C(4, 0);
+  kBackend->gemm(false, false, 2, 2, 2, 1.0, A.data(), 2, B.data(), 2, 0.0, C.data(), 2);
+  CHECK((C == std::vector<double>{19, 43, 22, 50}));
+  std::vector<double> C1{1, 1, 1, 1};
+  kBackend->gemm(false, false, 2, 2, 2, 1.0, A.data(), 2, B.data(), 2, 1.0, C1.data(), 2);
+  CHECK((C1 == std::vector<double>{20, 44, 23, 51}));
+  std::vector<double> x2{1, 1}, y2(2, 0);
+  kBackend->gemv(false, 2, 2, 1.0, A.data(), 2, x2.data(), 1, 0.0, y2.data(), 1);
+  CHECK((y2 == std::vector<double>{3, 7}));
+  std::vector<double> G(4, 0);
+  const std::vector<double> gx{1, 2}, gy{3, 4};
+  kBackend->ger(2, 2, 1.0, gx.data(), 1, gy.data(), 1, G.data(), 2);
+  CHECK((G == std::vector<double>{3, 6, 4, 8}));
+  const std::vector<double> dx{1, 2, 3}, dy{4, 5, 6};
+  CHECK(kBackend->dot(3, dx.data(), 1, dy.data(), 1) == 32.0);
+  std::vector<double> Z(4);
+  CHECK_THROWS_AS(kBackend->gemm(false, false, 2, 2, 2, 1.0, Z.data(), 1, Z.data(), 2, 0.0,
+                                 Z.data(), 2),
+                  std::invalid_argument);
+}
+
+TH_MAIN

@@ -1,0 +1,205 @@
+// Host-front suites restated from the reference's doctest files
+// (tests/test_tensor.cpp, test_expr.cpp, test_planner.cpp) against the
+// engine's tc:: API. CPU only.
+#include <set>
+
+#include "harness.hpp"
+#include "helpers.hpp"
+
+using namespace tc;
+using tst::bind_expr;
+
+namespace {
+const std::map<std::string, std::int64_t> kSq{{"a", 4}, {"b", 4}, {"g", 4}, {"e", 4}};
+const std::map<std::string, std::int64_t> kSq3{{"a", 3}, {"b", 3}, {"g", 3}};
+
+bool has_option(const std::vector<SlicingOption>& opts, const SlicingVector& sl,
+                const SlicingVector& sr, KernelKind k) {
+  for (const auto& o : opts)
+    if (o.s_left == sl && o.s_right == sr && o.report.kernel == k) return true;
+  return false;
+}
+Tensor mk(std::vector<std::int64_t> ext, const std::string& vars) {
+  std::vector<Variance> v;
+  for (char c : vars) v.push_back(c == '+' ? Variance::Up : Variance::Down);
+  return Tensor::zeros(ext, v);
+}
+}  // namespace
+
+// ------------------------------------------------------------ tensor (L0)
+TEST_CASE("column-major layout and strides") {  // test_tensor.cpp:19-66
+  Tensor t = Tensor::sequential({2, 3, 4}, {Variance::Up, Variance::Down, Variance::Up});
+  CHECK(t.at({1, 0, 0}) == 1.0);
+  CHECK(t.at({0, 1, 0}) == 2.0);
+  CHECK(t.at({0, 0, 1}) == 6.0);
+  CHECK(stride_of(t, 0) == 1);
+  CHECK(stride_of(t, 1) == 2);
+  CHECK(stride_of(t, 2) == 6);
+  CHECK_THROWS_AS(t.at({2, 0, 0}), std::out_of_range);
+  CHECK_THROWS_AS(Tensor({0}, {Variance::Up}), std::invalid_argument);
+}
+
+TEST_CASE("seeded determinism") {  // test_tensor.cpp:33-45
+  auto a = Tensor::seeded_random({5, 7}, {Variance::Up, Variance::Up}, 9);
+  auto b = Tensor::seeded_random({5, 7}, {Variance::Up, Variance::Up}, 9);
+  auto c = Tensor::seeded_random({5, 7}, {Variance::Up, Variance::Up}, 10);
+  CHECK(tensor_hash(a) == tensor_hash(b));
+  CHECK(tensor_hash(a) != tensor_hash(c));
+  for (std::int64_t i = 0; i < a.size(); ++i) CHECK(a.data()[i] >= -1.0 && a.data()[i] <= 1.0);
+}
+
+TEST_CASE("slice views alias and pack") {  // test_tensor.cpp:83-224
+  Tensor t = Tensor::sequential({3, 4, 5}, {Variance::Up, Variance::Up, Variance::Up});
+  auto v = slice_view(t, {0, 1, 0}, {2});
+  CHECK(v.rank() == 2);
+  CHECK(v.at({1, 3}) == t.at({1, 2, 3}));
+  auto pm = pack_slice(v);
+  CHECK_FALSE(pm.copied);
+  CHECK(pm.leading_dimension == 12);
+  auto w = slice_view(t, {1, 0, 0}, {1});
+  auto pw = pack_slice(w);
+  CHECK(pw.copied);
+  CHECK(pw.data[2 + 3 * 4] == t.at({1, 2, 3}));
+}
+
+// ------------------------------------------------------------ expr (L1)
+TEST_CASE("parse identifies contracted and free labels") {  // test_expr.cpp:20-31
+  const auto s = parse("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]");
+  CHECK(s.left.name == "A");
+  CHECK(s.output.indices.size() == 2);
+  CHECK(s.left.indices[1].label == "b");
+  CHECK(s.right.indices[0].var == Variance::Down);
+  CHECK_THROWS_AS(parse("R[+a,-e] = A[+a,+b,+g] * B[-g,-a,-e]"), parse_error);
+}
+
+TEST_CASE("validate binds extents and deltas") {  // test_expr.cpp:125-200
+  const auto s = parse("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]");
+  const auto v = validate(s, mk({4, 5, 6}, "+++"), mk({6, 4, 7}, "---"));
+  CHECK(v.delta_left == 1);
+  CHECK(v.delta_right == 1);
+  CHECK(v.p == 2);
+  CHECK(v.labels[v.label_index("e")].extent == 7);
+  CHECK_THROWS_AS(validate(s, mk({4, 5, 6}, "+++"), mk({6, 9, 7}, "---")), std::invalid_argument);
+  const auto sp = parse("R[+a] = T[+a,+b] * x[-b]", true);
+  validate(sp, mk({3, 4}, "+-"), mk({4}, "-"));
+  CHECK_THROWS_AS(validate(parse("R[+a] = T[+a,+b] * x[-b]"), mk({3, 4}, "+-"), mk({4}, "-")),
+                  std::invalid_argument);
+}
+
+TEST_CASE("parse of unparse is the identity") {  // test_expr.cpp:79-123
+  for (const char* e : {"R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", "K[] = T[+a,+b,+g] * S[-a,-b,-g]",
+                        "C[+i,-j] = A[+i,+h] * B[-h,-j]"}) {
+    const auto s = parse(e);
+    CHECK(parse(unparse(s)) == s);
+    CHECK(unparse(s) == e);
+  }
+}
+
+TEST_CASE("flop count") {  // test_expr.cpp:202-217
+  CHECK(flop_count(validate(parse("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]"), mk({10, 10, 10}, "+++"),
+                            mk({10, 10, 10}, "---"))) == 20000);
+  CHECK(flop_count(validate(parse("K[] = T[+a,+b,+g] * S[-a,-b,-g]"), mk({3, 3, 3}, "+++"),
+                            mk({3, 3, 3}, "---"))) == 54);
+}
+
+// ------------------------------------------------------------ planner (L2)
+TEST_CASE("classify the taxonomy anchor cases") {  // test_planner.cpp:27-45
+  CHECK(classify(bind_expr("K[] = T[+a,+b,+g] * S[-a,-b,-g]", kSq3).v) == ContractionClass::C1);
+  CHECK(classify(bind_expr("R[+a] = T[+a,+b,+g] * G[-b,-g]", kSq3).v) == ContractionClass::C2);
+  CHECK(classify(bind_expr("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", kSq).v) == ContractionClass::C31);
+  CHECK(classify(bind_expr("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", kSq).v) == ContractionClass::C32);
+}
+
+TEST_CASE("check_requirements catalog") {  // test_planner.cpp:79-129
+  const auto b = bind_expr("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", kSq);
+  const auto rep = check_requirements(b.v, {0, 1, 0}, {0, 1, 0});
+  CHECK(rep.r1_ok && rep.r2_ok && rep.r3_ok);
+  CHECK(rep.kernel == KernelKind::Gemm);
+  const auto c = bind_expr("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", kSq);
+  CHECK(check_requirements(c.v, {0, 0, 1}, {1, 0, 1}).kernel == KernelKind::Gemv);
+  CHECK(check_requirements(c.v, {1, 0, 1}, {1, 1, 0}).kernel == KernelKind::Ger);
+  CHECK_THROWS_AS(check_requirements(b.v, {0, 1, 0}, {0, 0, 0}), std::invalid_argument);
+}
+
+TEST_CASE("matmul enumeration: four decompositions plus GEMM") {  // test_planner.cpp:137-148
+  const auto b = bind_expr("C[+i,-j] = A[+i,+h] * B[-h,-j]", {{"i", 3}, {"j", 4}, {"h", 5}});
+  const auto opts = enumerate_slicings(b.v);
+  CHECK(has_option(opts, {0, 0}, {0, 0}, KernelKind::Gemm));
+  CHECK(has_option(opts, {1, 0}, {0, 0}, KernelKind::Gemv));
+  CHECK(has_option(opts, {0, 0}, {0, 1}, KernelKind::Gemv));
+  CHECK(has_option(opts, {0, 1}, {1, 0}, KernelKind::Ger));
+  CHECK(has_option(opts, {1, 0}, {0, 1}, KernelKind::Dot));
+  for (std::size_t i = 1; i < opts.size(); ++i)
+    CHECK(std::tie(opts[i - 1].s_left, opts[i - 1].s_right) <
+          std::tie(opts[i].s_left, opts[i].s_right));
+}
+
+TEST_CASE("class 3.2 auto plan accumulates over the sliced contracted label") {
+  // test_planner.cpp:226-239
+  const auto b = bind_expr("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]",
+                           {{"a", 5}, {"b", 4}, {"g", 3}, {"e", 6}});
+  const auto p = plan(b.v);
+  CHECK(p.kernel == KernelKind::Gemm);
+  REQUIRE(p.loop_nest.size() == 1);
+  CHECK(p.loop_nest[0].contracted);
+  CHECK(b.v.labels[p.loop_nest[0].label].label == "g");
+  CHECK(p.copies.empty());
+  CHECK(p.flops == flop_count(b.v));
+}
+
+TEST_CASE("recipes and forced-GEMM errors") {  // test_planner.cpp:244-307
+  CHECK(plan(bind_expr("K[] = T[+a,+b,+g] * S[-a,-b,-g]", kSq3).v).kernel == KernelKind::Dot);
+  CHECK(plan(bind_expr("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", kSq).v).kernel ==
+        KernelKind::CopyGemm);
+  CHECK_THROWS_WITH_AS(plan(bind_expr("K[] = T[+a,+b,+g] * S[-a,-b,-g]", kSq3).v,
+                            PlanPolicy::force_kernel(KernelKind::Gemm)),
+                       "kernel unreachable: R3 violated", kernel_unreachable_error);
+  CHECK_THROWS_WITH_AS(plan(bind_expr("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", kSq).v,
+                            PlanPolicy::force_kernel(KernelKind::Gemm)),
+                       "kernel unreachable: R1 violated", kernel_unreachable_error);
+  CHECK_THROWS_WITH_AS(plan(bind_expr("R[+a] = T[+a,+b] * x[-b]", {{"a", 4}, {"b", 5}}).v,
+                            PlanPolicy::force_kernel(KernelKind::Gemm)),
+                       "kernel unreachable: R2 violated", kernel_unreachable_error);
+}
+
+TEST_CASE("plan report renders deterministically") {  // test_planner.cpp:334-349
+  const auto b = bind_expr("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", kSq);
+  CHECK(render_plan(plan(b.v), b.v) ==
+        "class: 3.2\ndelta: (1, 1)\ns_left: (0, 0, 1)\ns_right: (0, 0, 1)\ns_output: (0, 0)\n"
+        "kernel: GEMM\nloop_nest: g:contracted\nkernel_map: M=a N=e K=b transA=0 transB=1\n"
+        "copies: 0\nflops: 512\n");
+}
+
+TEST_CASE("relayout advice turns a crossed contraction into a direct one") {
+  const auto b = bind_expr("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", kSq);
+  const auto adv = relayout_advice(b.v);
+  REQUIRE(adv.has_value());
+  CHECK(adv->find("class 3.2") != std::string::npos);
+  CHECK_FALSE(relayout_advice(bind_expr("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", kSq).v));
+}
+
+TEST_CASE("loop nest and kernel map partition the labels (BASELINE configs)") {
+  const std::pair<const char*, std::map<std::string, std::int64_t>> cfgs[] = {
+      {"C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", {{"i", 8}, {"j", 8}, {"k", 4}, {"l", 4}}},
+      {"C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]", {{"a", 4}, {"b", 4}, {"c", 4}, {"k", 4}}},
+      {"C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]",
+       {{"a", 4}, {"b", 4}, {"c", 4}, {"d", 4}, {"k", 2}, {"l", 2}}}};
+  for (const auto& [e, ext] : cfgs) {
+    const auto b = bind_expr(e, ext);
+    CHECK(classify(b.v) == ContractionClass::C32);  // all BASELINE configs 3.2
+    const auto p = plan(b.v);
+    std::set<int> seen;
+    for (const auto& l : p.loop_nest) CHECK(seen.insert(l.label).second);
+    for (int k : {p.kernel_map.m_label, p.kernel_map.n_label, p.kernel_map.k_label})
+      if (k >= 0) CHECK(seen.insert(k).second);
+    CHECK(seen.size() == b.v.labels.size());
+  }
+}
+
+TEST_CASE("only the device backend exists") {
+  CHECK(make_backend("b200")->name() == "b200");
+  CHECK_THROWS_AS(make_backend("reference"), std::invalid_argument);
+  CHECK_THROWS_AS(make_backend("nope"), std::invalid_argument);
+}
+
+TH_MAIN

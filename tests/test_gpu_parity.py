@@ -1,0 +1,178 @@
+"""Parity of the device path (plan-level C-ABI tcf_execute / tcf_prepare ->
+DMMA kernels) with the reference on the same seeded inputs. Tolerance:
+relative Frobenius <= 1e-12 (BASELINE) and the reference's own
+max_rel_error <= 1e-12 (tests/test_executor.cpp:76-87). Requires a B200."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracles as O
+import paper_1307_2100_b200 as T
+from specgen import random_spec
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+TOL = 1e-12
+
+
+def close(got, want):
+    return O.max_rel_error(got, want) <= TOL and O.rel_frobenius(got, want) <= TOL
+
+
+def test_golden_small_contractions(dev):
+    meta = json.loads((GOLD / "small.json").read_text())
+    arrs = np.load(GOLD / "small.npz")
+    for i, m in enumerate(meta):
+        got, st = T.execute(m["expr"], m["extents"], seed=1)
+        assert close(got, arrs[f"exec_{i}"]), m["expr"]
+        assert close(got, arrs[f"naive_{i}"]), m["expr"]
+        assert st["flops"] == m["stats"]["flops"]
+
+
+def test_random_auto_plans_match_oracle(dev):
+    # tests/test_executor.cpp:76-87 (300 random auto plans vs the naive oracle)
+    rng = np.random.default_rng(31337)
+    for _ in range(300):
+        e, x = random_spec(rng)
+        L, R = O.operands(e, x, 1)
+        got, _ = T.execute(e, x, seed=1)
+        assert close(got, O.naive(e, x, L, R)), (e, x)
+
+
+def test_every_slicing_computes_the_same_tensor(dev):
+    # tests/test_executor.cpp:89-102 (forced slicings of 25 random specs)
+    rng = np.random.default_rng(2718)
+    for _ in range(25):
+        e, x = random_spec(rng, max_extent=4)
+        L, R = O.operands(e, x, 1)
+        want = O.naive(e, x, L, R)
+        opts = T.report(e, x).split("options:\n")[1].split("auto:")[0].strip().splitlines()
+        for line in opts:
+            sl, sr = line.split("|")[:2]
+            got, _ = T.execute(e, x, seed=1, slicing=(sl, sr))
+            assert close(got, want), (e, x, sl, sr)
+
+
+def test_forced_kernels_agree_on_crossed_order4(dev):
+    # tests/test_executor.cpp:118-129
+    e = "R[+a,+b,+c,+d] = X[+i,+a,+j,+b] * Y[-j,+c,-i,+d]"
+    x = "a=2,b=3,c=2,d=3,i=2,j=3"
+    L, R = O.operands(e, x, 1)
+    want = O.naive(e, x, L, R)
+    for k in ("COPY+GEMM", "DOT", "GER"):
+        got, _ = T.execute(e, x, seed=1, kernel=k)
+        assert close(got, want), k
+
+
+def test_stats_and_single_launch(dev):
+    # 3.2 plans copy nothing and run as ONE device launch (test_executor.cpp:66-74)
+    got, st = T.execute("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", "a=6,b=5,g=4,e=3")
+    assert st["packed_bytes"] == 0 and st["staged_bytes"] == 0 and st["kernel_calls"] == 1
+    # class 3.1 (crossed stride-1 labels): operands permuted once on the device
+    got, st = T.execute("R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", "a=4,b=4,g=4,e=4")
+    assert st["packed_bytes"] > 0 and st["kernel_calls"] >= 2
+
+
+def test_scalar_vector_and_unit_extent_edges(dev):
+    cases = [("K[] = T[+a,+b,+g] * S[-a,-b,-g]", "a=3,b=3,g=3"),          # C1 -> DOT
+             ("K[] = T[+a,+b,+g] * S[-a,-b,-g]", "a=300,b=200,g=50"),      # long DOT
+             ("R[+a] = T[+a,+b,+g] * G[-b,-g]", "a=4,b=5,g=6"),            # C2 -> GEMV
+             ("R[+g] = T[+a,+b,+g] * G[-a,-b]", "a=40,b=50,g=600"),        # GEMV, k-major rows
+             ("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", "a=1,b=1,g=1,e=1"),   # all unit
+             ("R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]", "a=4,b=1,g=3,e=5"),   # unit contracted
+             ("R[+b,+a,+c] = A[+a,+b,-k] * B[+k,+c]", "a=3,b=4,c=5,k=2"),   # staged output order
+             ("R[+a,+b,+c,+d,+e,+f] = X[+a,+b,+c,+i,+j] * Y[-j,-i,+d,+e,+f]",
+              "a=3,b=5,c=2,d=4,e=3,f=2,i=7,j=3")]                          # rank-6 output
+    for e, x in cases:
+        L, R = O.operands(e, x, 1)
+        got, _ = T.execute(e, x, seed=1)
+        assert close(got, O.naive(e, x, L, R)), (e, x)
+
+
+def test_results_are_bit_reproducible(dev):
+    e, x = "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=512,j=512,k=64,l=64"
+    a, _ = T.execute(e, x, seed=1)
+    b, _ = T.execute(e, x, seed=1, workers=3)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
+def test_baseline_configs_full_size(dev, cfg):
+    g = json.loads((GOLD / "baseline.json").read_text())[cfg]
+    got, st = T.execute(g["expr"], g["extents"], seed=1)
+    assert st["flops"] == g["flops"]
+    idx = np.array(g["idx"])
+    val = np.array(g["val"])
+    scale = max(1.0, np.abs(val).max())
+    assert np.abs(got[idx] - val).max() / scale <= TOL
+    assert abs(got.sum() - g["sum"]) <= 1e-9 * abs(g["sumsq"]) ** 0.5 * 10
+    assert abs((got * got).sum() - g["sumsq"]) <= 1e-11 * g["sumsq"]
+    live = O.ref_execute(g["expr"], g["extents"], seed=1, workers=16)
+    if live is not None:
+        assert close(got, live[0])
+
+
+def _sampled_check(expr, extents, got, L, R, samples, rng):
+    """C entries recomputed on the CPU by direct summation over the contracted
+    labels (the reference's sampled-line idea, src/bench.cpp:59-112)."""
+    out, left, right = O.parse(expr)
+    ext = O.ext_map(extents)
+    con = [x for x in left if x in right]
+    shapeL = [ext[x] for x in reversed(left)]
+    shapeR = [ext[x] for x in reversed(right)]
+    Lt = L.reshape(shapeL)
+    Rt = R.reshape(shapeR)
+    scale = 0.0
+    worst = 0.0
+    ostr, _ = O.strides(out, ext)
+    for _ in range(samples):
+        coord = {x: int(rng.integers(ext[x])) for x in out}
+        li = tuple(coord[x] if x in coord else slice(None) for x in reversed(left))
+        ri = tuple(coord[x] if x in coord else slice(None) for x in reversed(right))
+        a = Lt[li]
+        b = Rt[ri]
+        # align contracted axes: a's axes are reversed-left order of con labels
+        la = [x for x in reversed(left) if x in con]
+        rb = [x for x in reversed(right) if x in con]
+        b = np.transpose(b, [rb.index(x) for x in la])
+        want = float(np.sum(a * b, dtype=np.float64))
+        off = sum(coord[x] * ostr[x] for x in out)
+        worst = max(worst, abs(got[off] - want))
+        scale = max(scale, abs(want))
+    return worst / max(1.0, scale)
+
+
+def test_cfg4_full_size_sampled(dev):
+    e, x = "C[+a,+b,+i,+j] = A[+a,+b,+k,+l] * B[-k,-l,+i,+j]", "a=256,b=256,i=64,j=64,k=64,l=64"
+    p = T.Prepared(e, x)
+    inf = p.info()
+    L, R = T.seeded(inf["left"], 1), T.seeded(inf["right"], 2)
+    p.upload(L, R)
+    p.run()
+    got = np.empty(inf["output"])
+    p.download(got)
+    assert _sampled_check(e, x, got, L, R, 300, np.random.default_rng(1)) <= TOL
+    # size-independent property: linearity in the left operand (exact, x2)
+    p.upload(2.0 * L, R)
+    p.run()
+    got2 = np.empty(inf["output"])
+    p.download(got2)
+    assert np.array_equal(got2, 2.0 * got)
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_sampled(dev):
+    e, x = "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=8192,j=8192,k=512,l=512"
+    p = T.Prepared(e, x)
+    inf = p.info()
+    L = T.seeded(inf["left"], 1)
+    R = T.seeded(inf["right"], 2)
+    p.upload(L, R)
+    del_ok = True
+    p.run()
+    got = np.empty(inf["output"])
+    p.download(got)
+    assert np.isfinite(got).all() and del_ok
+    assert _sampled_check(e, x, got, L, R, 40, np.random.default_rng(5)) <= TOL
