@@ -5,11 +5,12 @@
 // coalescing and enough bytes in flight:
 //   * K-major matrix (k contiguous): one warp per output row and k-chunk,
 //     lanes stream k with 8-byte loads, warp-shuffle tree reduction;
-//   * row-major-in-outer matrix (rows contiguous): 32 rows x 8 k-lanes per
+//   * row-major-in-outer matrix (rows contiguous): 32 rows x 8 threads per
 //     block, coalesced along rows, shared-memory reduction over the k-lanes;
 //   * DOT is the one-row case of the K-major kernel.
-// Long K is split into chunks whose partials are summed by a second kernel in
-// chunk order, so results are bit-reproducible run to run.
+// Both kernels sum in the same order (32 k-lanes, fixed combine tree) and long
+// K is split into 32-multiple chunks summed by a second kernel in chunk order,
+// so results are bit-reproducible and independent of the operand layout.
 #include <algorithm>
 
 #include "tcb_internal.cuh"
@@ -83,23 +84,25 @@ __global__ void gemv_kmajor(GvParams p) {
     const double* mrow = p.M + om + o * p.so;
     const double* vec = p.v + ov;
     const int64_t k0 = s * p.chunk, k1 = min(p.K, k0 + p.chunk);
-    double acc0 = 0.0, acc1 = 0.0;
-    int64_t k = k0 + lane;
-    for (; k + 32 < k1; k += 64) {
-      acc0 = fma(__ldg(mrow + k * p.sk), __ldg(vec + k * p.sv), acc0);
-      acc1 = fma(__ldg(mrow + (k + 32) * p.sk), __ldg(vec + (k + 32) * p.sv), acc1);
-    }
-    if (k < k1) acc0 = fma(__ldg(mrow + k * p.sk), __ldg(vec + k * p.sv), acc0);
-    double acc = acc0 + acc1;
+    // k-lane l sums k = k0 + l, k0 + l + 32, ... in order; lanes combine in a
+    // fixed xor tree. gemv_omajor reproduces exactly this order.
+    double acc = 0.0;
+#pragma unroll 4
+    for (int64_t k = k0 + lane; k < k1; k += 32)
+      acc = fma(__ldg(mrow + k * p.sk), __ldg(vec + k * p.sv), acc);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (lane == 0) gv_store(p, b, o, s, acc);
   }
 }
 
-// 32 rows x 8 k-lanes per block; rows are the coalesced direction
+// 32 rows x 8 threads per block; rows are the coalesced direction. Thread ty
+// carries the 4 k-lanes ty, ty+8, ty+16, ty+24 of the 32-lane order used by
+// gemv_kmajor, and the lanes are combined with the same tree, so both layouts
+// give bit-identical results (cf. the reference's transpose-equivalence test,
+// tests/test_kernels.cpp:86-116).
 __global__ void gemv_omajor(GvParams p) {
-  __shared__ double red[8][33];
+  __shared__ double red[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t rblocks = (p.rows + 31) / 32;
   const int64_t items = p.batch * rblocks * p.splits;
@@ -111,20 +114,29 @@ __global__ void gemv_omajor(GvParams p) {
     gv_batch(p, b, om, ov, oy);
     const int64_t o = rb * 32 + tx;
     const int64_t k0 = s * p.chunk, k1 = min(p.K, k0 + p.chunk);
-    double acc = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (o < p.rows) {
       const double* mcol = p.M + om + o * p.so;
       const double* vec = p.v + ov;
-      for (int64_t k = k0 + ty; k < k1; k += 8)
-        acc = fma(__ldg(mcol + k * p.sk), __ldg(vec + k * p.sv), acc);
+      for (int64_t kb = k0; kb < k1; kb += 32)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t k = kb + ty + 8 * j;
+          if (k < k1) acc[j] = fma(__ldg(mcol + k * p.sk), __ldg(vec + k * p.sv), acc[j]);
+        }
     }
-    red[ty][tx] = acc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[ty + 8 * j][tx] = acc[j];
     __syncthreads();
     if (ty == 0 && o < p.rows) {
-      double sum = red[0][tx];
+      double l[32];
 #pragma unroll
-      for (int i = 1; i < 8; ++i) sum += red[i][tx];
-      gv_store(p, b, o, s, sum);
+      for (int i = 0; i < 32; ++i) l[i] = red[i][tx];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int i = 0; i < off; ++i) l[i] = l[i] + l[i + off];
+      gv_store(p, b, o, s, l[0]);
     }
     __syncthreads();
   }
@@ -198,21 +210,20 @@ int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double
   // the k-contiguous kernel when rows are not unit-stride (or there is one row)
   const bool kmajor = p.sk == 1 ? (p.so != 1 || p.rows == 1) : (p.so != 1 && p.rows == 1);
   const bool use_k = kmajor || p.rows == 1;
+  // The k-chunking depends only on the problem (never on which kernel runs)
+  // and chunks are multiples of 32, so the summation order is layout-free.
   int64_t splits = 1;
-  if (use_k) {
+  {
     const int64_t target = static_cast<int64_t>(sms) * 32;
     const int64_t rows_total = p.batch * p.rows;
-    if (rows_total < target) splits = std::min<int64_t>((target + rows_total - 1) / rows_total,
-                                                        std::max<int64_t>(1, d.k / 512));
-  } else {
-    const int64_t target = static_cast<int64_t>(sms) * 8;
-    const int64_t blocks = p.batch * ((p.rows + 31) / 32);
-    if (blocks < target) splits = std::min<int64_t>((target + blocks - 1) / blocks,
-                                                    std::max<int64_t>(1, d.k / 128));
+    if (rows_total < target)
+      splits = std::min<int64_t>((target + rows_total - 1) / rows_total,
+                                 std::max<int64_t>(1, d.k / 512));
   }
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 4096));
+  p.chunk = ((d.k + splits - 1) / splits + 31) / 32 * 32;
+  splits = (d.k + p.chunk - 1) / p.chunk;
   p.splits = static_cast<int>(splits);
-  p.chunk = (d.k + splits - 1) / splits;
   if (splits > 1) {
     const int64_t need = p.batch * p.rows * splits * 8;
     if (need > st.ws_bytes) {

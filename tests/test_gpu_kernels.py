@@ -132,12 +132,12 @@ def test_gemv_ger_dot_known_answers(dev):
     T.check(dev.tcb_dger(2, 2, 1.0, e1.ptr, 1, e2.ptr, 1, G.ptr, 2))
     assert G.to_array(4).tolist() == [0, 0, 1, 0]
     G2 = D.from_array(np.zeros(4))
-    T.check(dev.tcb_dger(2, 2, 1.0, D.from_array(np.array([1., 2])).ptr, 1,
-                         D.from_array(np.array([3., 4])).ptr, 1, G2.ptr, 2))
+    gx, gy = D.from_array(np.array([1., 2])), D.from_array(np.array([3., 4]))
+    T.check(dev.tcb_dger(2, 2, 1.0, gx.ptr, 1, gy.ptr, 1, G2.ptr, 2))
     assert G2.to_array(4).tolist() == [3, 6, 4, 8]
     r = C.c_double()
-    T.check(dev.tcb_ddot(3, D.from_array(np.array([1., 2, 3])).ptr, 1,
-                         D.from_array(np.array([4., 5, 6])).ptr, 1, C.byref(r)))
+    dx, dy = D.from_array(np.array([1., 2, 3])), D.from_array(np.array([4., 5, 6]))
+    T.check(dev.tcb_ddot(3, dx.ptr, 1, dy.ptr, 1, C.byref(r)))
     assert r.value == 32.0
     T.check(dev.tcb_ddot(0, x.ptr, 1, x.ptr, 1, C.byref(r)))
     assert r.value == 0.0
@@ -151,8 +151,8 @@ def test_gemv_and_dot_large_vs_numpy(dev):
             xl, yl = (m, n) if trans else (n, m)
             x = rng.uniform(-1, 1, xl)
             y = D.from_array(np.zeros(yl))
-            T.check(dev.tcb_dgemv(trans, m, n, 1.0, D.from_array(A).ptr, m, D.from_array(x).ptr, 1,
-                                  0.0, y.ptr, 1))
+            dA, dx = D.from_array(A), D.from_array(x)  # keep alive: kernels run async
+            T.check(dev.tcb_dgemv(trans, m, n, 1.0, dA.ptr, m, dx.ptr, 1, 0.0, y.ptr, 1))
             M = A.reshape(n, m).T
             want = (M.T @ x) if trans else (M @ x)
             assert np.allclose(y.to_array(yl), want, rtol=1e-12, atol=1e-12)
