@@ -70,6 +70,7 @@ struct Params {
   int64_t units;
   double* ws;
   unsigned* counters;
+  unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
   // TMA: tensor-map rank and which batch dims each map carries.
   int a_rank, b_rank;
   int a_bdim[3], b_bdim[3];
@@ -294,7 +295,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t s_base = smem_u32(smem);
   const uint32_t full0 = smem_u32(bars);            // full[s]  = full0 + 8s
   const uint32_t empty0 = smem_u32(bars + STAGES);  // empty[s] = empty0 + 8s
-  volatile unsigned* s_flag = reinterpret_cast<volatile unsigned*>(bars + 2 * STAGES);
   // per-tile output offsets: composite row(m) / col(n) of the tile, -1 = outside C
   int64_t* s_row = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + 256);
   int64_t* s_col = s_row + BM;
@@ -403,49 +403,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     // ------------------------------ epilogue ------------------------------
-    if (p.splits > 1) {
-      const int64_t tile = u / p.splits;
-      double* part = p.ws + (tile * p.splits + un.split) * static_cast<int64_t>(BM * BN);
-#pragma unroll
-      for (int im = 0; im < 8; ++im)
-#pragma unroll
-        for (int in = 0; in < 4; ++in) {
-          const int v = im * 4 + in;
-          __stcg(reinterpret_cast<double2*>(part) + v * CTHREADS + ctid,
-                 make_double2(acc[im][in][0], acc[im][in][1]));
-        }
-      __threadfence();
-      consumer_sync();
-      if (ctid == 0) {
-        const unsigned prev = atomicAdd(p.counters + tile, 1u);
-        *s_flag = (prev == static_cast<unsigned>(p.splits - 1)) ? 1u : 0u;
-      }
-      consumer_sync();
-      const bool last = *s_flag != 0u;
-      consumer_sync();      // s_flag is reused by the next unit
-      if (!last) continue;  // not the last split of this tile
-      __threadfence();
-      const double* base = p.ws + tile * p.splits * static_cast<int64_t>(BM * BN);
-#pragma unroll
-      for (int im = 0; im < 8; ++im)
-#pragma unroll
-        for (int in = 0; in < 4; ++in) acc[im][in][0] = acc[im][in][1] = 0.0;
-#pragma unroll 1
-      for (int s = 0; s < p.splits; ++s) {
-        const double2* ps =
-            reinterpret_cast<const double2*>(base + s * static_cast<int64_t>(BM * BN));
-#pragma unroll
-        for (int im = 0; im < 8; ++im)
-#pragma unroll
-          for (int in = 0; in < 4; ++in) {
-            const double2 v = __ldcg(ps + (im * 4 + in) * CTHREADS + ctid);
-            acc[im][in][0] += v.x;
-            acc[im][in][1] += v.y;
-          }
-      }
-      if (ctid == 0) p.counters[tile] = 0u;  // re-arm for the next launch
-    }
-
     // Output offsets of this tile's 128 rows and 128 columns, decoded once
     // (one composite index per consumer thread) into shared memory.
     consumer_sync();  // the previous unit's epilogue is done with the tables
@@ -462,14 +419,88 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int bc[TCB_MAX_DIMS];
     int64_t oa, ob, oc;
     batch_offsets(p, un.batch, oa, ob, oc, bc);
+    double* Cb = p.C + oc;
+    const bool use_beta = p.beta != 0.0;
+
+    if (p.splits > 1) {
+      // Split-K (cooperative launch: all splits of a tile are co-resident).
+      // 1) every split stores its partial tile ([n][m], m contiguous);
+      // 2) the splits meet at a per-tile arrival counter;
+      // 3) split s reduces elements [s*T/S, (s+1)*T/S) of the tile, summing
+      //    the S partials in split order — bit-reproducible, and the
+      //    reduction is spread over all S CTAs instead of one.
+      const int64_t tile = u / p.splits;
+      double* base = p.ws + tile * p.splits * static_cast<int64_t>(BM * BN);
+      double* part = base + un.split * static_cast<int64_t>(BM * BN);
+#pragma unroll
+      for (int im = 0; im < 8; ++im)
+#pragma unroll
+        for (int in = 0; in < 4; ++in)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            __stcg(part + (wn * 32 + in * 8 + 2 * q + jj) * BM + wm * 64 + im * 8 + r,
+                   acc[im][in][jj]);
+      __threadfence();
+      consumer_sync();
+      if (ctid == 0) {
+        atomicAdd(p.counters + tile, 1u);
+        const unsigned target = (p.epoch + 1u) * static_cast<unsigned>(p.splits);
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.counters + tile)
+                       : "memory");
+          if (seen < target) __nanosleep(64);
+        } while (seen < target);
+      }
+      consumer_sync();
+      const int e0 = (BM * BN) * un.split / p.splits;
+      const int e1 = (BM * BN) * (un.split + 1) / p.splits;
+      // Each thread owns up to RED_ELEMS elements of the slice and issues all
+      // their S partial loads before summing (one L2 round trip, not S).
+      constexpr int RED_ELEMS = 8;
+#pragma unroll 1
+      for (int eb = e0 + ctid; eb < e1; eb += CTHREADS * RED_ELEMS) {
+        double sum[RED_ELEMS];
+#pragma unroll
+        for (int i = 0; i < RED_ELEMS; ++i) sum[i] = 0.0;
+#pragma unroll 1
+        for (int sp0 = 0; sp0 < p.splits; sp0 += 4) {
+          double v[4][RED_ELEMS];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < RED_ELEMS; ++i) {
+              const int e = eb + i * CTHREADS;
+              v[j][i] = (sp0 + j < p.splits && e < e1)
+                            ? __ldcg(base + (sp0 + j) * (BM * BN) + e) : 0.0;
+            }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < RED_ELEMS; ++i)
+              if (sp0 + j < p.splits) sum[i] += v[j][i];  // split order 0..S-1
+        }
+#pragma unroll
+        for (int i = 0; i < RED_ELEMS; ++i) {
+          const int e = eb + i * CTHREADS;
+          if (e >= e1) continue;
+          const int64_t roff = s_row[e & (BM - 1)], coff = s_col[e >> 7];
+          if (roff < 0 || coff < 0) continue;
+          double* dst = Cb + roff + coff;
+          double vv = p.alpha * sum[i];
+          if (use_beta) vv += p.beta * *dst;
+          *dst = vv;
+        }
+      }
+      continue;
+    }
+
     consumer_sync();
     int64_t coff[4][2];
 #pragma unroll
     for (int in = 0; in < 4; ++in)
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) coff[in][jj] = s_col[wn * 32 + in * 8 + 2 * q + jj];
-    double* Cb = p.C + oc;
-    const bool use_beta = p.beta != 0.0;
 #pragma unroll
     for (int im = 0; im < 8; ++im) {
       const int64_t roff = s_row[wm * 64 + im * 8 + r];
@@ -584,8 +615,17 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(p, ta, tb);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // split-K CTAs wait on each other
+  attr[0].val.cooperative = p.splits > 1 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p, ta, tb);
 }
 
 }  // namespace
@@ -656,7 +696,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   int splits = 1;
   if (tiles < sms) {
     splits = static_cast<int>(std::min<int64_t>(sms / tiles, std::max<int64_t>(1, kblocks / 8)));
-    splits = std::max(1, splits);
+    splits = std::max(1, std::min(splits, 16));
   }
   p.splits = splits;
   p.units = tiles * splits;
@@ -670,16 +710,25 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       TCB_CUDA(cudaMalloc(&st.ws, need));
       st.ws_bytes = need;
     }
+    // Per-tile arrival counters grow by `splits` per launch (epoch); they are
+    // re-zeroed whenever the (tiles, splits) shape changes, after a failed
+    // launch, on reallocation and long before they could wrap.
     if (tiles > st.counters_n) {
       if (st.counters) cudaFree(st.counters);
       st.counters = nullptr;
       st.counters_n = 0;
       TCB_CUDA(cudaMalloc(&st.counters, tiles * sizeof(unsigned)));
-      TCB_CUDA(cudaMemsetAsync(st.counters, 0, tiles * sizeof(unsigned), st.stream));
       st.counters_n = tiles;
+      st.last_splits = 0;
+    }
+    if (st.last_splits != splits || st.last_tiles != tiles ||
+        static_cast<int64_t>(st.epoch + 2) * splits >= (1LL << 31)) {
+      TCB_CUDA(cudaMemsetAsync(st.counters, 0, st.counters_n * sizeof(unsigned), st.stream));
+      st.epoch = 0;
     }
     p.ws = static_cast<double*>(st.ws);
     p.counters = st.counters;
+    p.epoch = st.epoch;
   }
 
   // Operand layouts: MN-major when the outer index is unit-stride.
@@ -707,8 +756,16 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     else if (b_k) e = launch_one<false, true, false>(p, ta, tb, grid, st.stream);
     else e = launch_one<false, false, false>(p, ta, tb, grid, st.stream);
   }
-  if (e != cudaSuccess) return cuda_fail(e, "dgemm_dmma launch");
+  if (e != cudaSuccess) {
+    st.last_splits = 0;
+    return cuda_fail(e, "dgemm_dmma launch");
+  }
   ++st.launches;
+  if (splits > 1) {
+    ++st.epoch;  // the counters of these tiles now hold epoch*splits
+    st.last_splits = splits;
+    st.last_tiles = tiles;
+  }
   st.last_info.path = tma ? 0 : 1;
   st.last_info.splits = splits;
   st.last_info.units = p.units;

@@ -19,8 +19,11 @@ struct ThreadState {
   cudaStream_t stream = nullptr;  // own_stream or a caller stream
   void* ws = nullptr;             // split-K partials
   int64_t ws_bytes = 0;
-  unsigned* counters = nullptr;   // per-tile arrival counters (kept zeroed)
+  unsigned* counters = nullptr;   // split-K per-tile arrival counters
   int64_t counters_n = 0;
+  unsigned epoch = 0;             // split-K launches since the counters were zeroed
+  int last_splits = 0;             // (tiles, splits) of the last split-K launch
+  int64_t last_tiles = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   tcb_gemm_info last_info{};
