@@ -4,14 +4,16 @@
 // the CPU, once per kernel call (materialize, src/executor.cpp:41-59; also
 // pack_slice, src/tensor.cpp:150-171). Here a whole operand is re-laid out once
 // per contraction, HBM-bound, in one launch:
-//   * same unit-stride dim in source and destination -> run copy: one warp per
-//     contiguous run, 16-byte vector loads/stores when aligned;
-//   * different unit-stride dims -> 32x32 shared-memory tiled transpose
-//     (padded, conflict-free), remaining dims on the grid;
+//   * same unit-stride dim in source and destination -> run copy: blocks walk
+//     chunks of contiguous runs (offsets decoded once per block item), 16-byte
+//     vectors, 4 in flight per thread;
+//   * different unit-stride dims -> 32x64 shared-memory tiled transpose
+//     (padded), 8 loads in flight per thread, remaining dims on the grid;
 //   * no unit-stride source dim -> element-wise gather (rare, small).
 // Dimensions are first simplified: extent-1 dims dropped, dims that are
 // contiguous in both layouts merged.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "tcb_internal.cuh"
@@ -26,7 +28,8 @@ struct PermParams {
   int64_t ext[MAXR];        // destination order, first fastest
   int64_t sstr[MAXR];       // source strides per dim
   int64_t dstr[MAXR];       // destination strides (dense)
-  int t;                    // transpose: the source unit-stride dim
+  int t;                    // transpose: the source unit-stride dim; runs: log2(run) or -1
+  int64_t runs_per_chunk;   // runs: dim-1 runs handled by one block item
   int64_t rows;             // run copy: number of runs / transpose: number of outer slabs
   int outer_n;              // dims enumerated by the grid (all but 0 [and t])
   int outer_dim[MAXR];
@@ -45,52 +48,78 @@ __device__ __forceinline__ void outer_offsets(const PermParams& p, int64_t idx, 
   }
 }
 
-// Same unit-stride dim: copy runs of ext[0] contiguous doubles.
+// Same unit-stride dim: copy runs of ext[0] contiguous doubles. One block
+// per "slab" = all ext[1] runs at one coordinate of the outer dims (decoded
+// once per block); inside a slab run r starts at r*sstr[1] (source) and
+// r*ext[0] (destination), so no per-element index decoding. Each thread keeps
+// UNROLL 16-byte vectors in flight (loads first, then stores).
 template <bool VEC>
 __global__ void perm_runs(PermParams p, const double* __restrict__ src, double* __restrict__ dst) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const int64_t L = p.ext[0];
-  for (int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
-       row < p.rows; row += warps) {
+  constexpr int UNROLL = 4;
+  using V = typename std::conditional<VEC, double2, double>::type;
+  constexpr int W = VEC ? 2 : 1;  // doubles per vector
+  const int64_t L = p.ext[0] / W;  // vectors per run
+  const int64_t runs = p.rank > 1 ? p.ext[1] : 1;
+  const int64_t rpc = p.runs_per_chunk;
+  const int64_t chunks = (runs + rpc - 1) / rpc;
+  const int lshift = p.t;  // log2(L) when L is a power of two, else -1
+  for (int64_t item = blockIdx.x; item < p.rows * chunks; item += gridDim.x) {
+    const int64_t slab = item / chunks, r0 = (item % chunks) * rpc;
+    const int64_t per_slab = L * min(rpc, runs - r0);
     int64_t so, dof;
-    outer_offsets(p, row, so, dof);
-    const double* s = src + so;
-    double* d = dst + dof;
-    if (VEC) {
-      const double2* s2 = reinterpret_cast<const double2*>(s);
-      double2* d2 = reinterpret_cast<double2*>(d);
-      for (int64_t i = lane; i < L / 2; i += 32) __stcs(d2 + i, __ldcs(s2 + i));
-    } else {
-      for (int64_t i = lane; i < L; i += 32) __stcs(d + i, __ldcs(s + i));
+    outer_offsets(p, slab, so, dof);
+    const int64_t rs = p.rank > 1 ? p.sstr[1] / W : 0;  // run stride in vectors
+    const V* s = reinterpret_cast<const V*>(src + so) + r0 * rs;
+    V* d = reinterpret_cast<V*>(dst + dof) + r0 * L;
+    for (int64_t base = threadIdx.x; base < per_slab; base += blockDim.x * UNROLL) {
+      V v[UNROLL];
+      int64_t di[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t i = base + u * blockDim.x;
+        di[u] = i;
+        if (i < per_slab) {
+          const int64_t r = lshift >= 0 ? (i >> lshift) : i / L;
+          const int64_t c = i - r * L;
+          v[u] = __ldcs(s + r * rs + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (di[u] < per_slab) __stcs(d + di[u], v[u]);
     }
   }
 }
 
-// Different unit-stride dims: transpose tiles of (dst dim 0) x (src dim t).
-__global__ void perm_transpose(PermParams p, const double* __restrict__ src,
-                               double* __restrict__ dst) {
-  __shared__ double tile[32][33];
+// Different unit-stride dims: transpose tiles of 32 (dst dim 0) x 64 (src
+// dim t) through padded shared memory; every thread issues its 8 loads before
+// the barrier and its 8 stores after it (both directions coalesced).
+__global__ void __launch_bounds__(256) perm_transpose(PermParams p, const double* __restrict__ src,
+                                                      double* __restrict__ dst) {
+  __shared__ double tile[32][65];
   const int64_t e0 = p.ext[0], et = p.ext[p.t];
-  const int64_t t0n = (e0 + 31) / 32, ttn = (et + 31) / 32;
+  const int64_t t0n = (e0 + 31) / 32, ttn = (et + 63) / 64;
   const int64_t tiles = t0n * ttn * p.rows;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   for (int64_t b = blockIdx.x; b < tiles; b += gridDim.x) {
     const int64_t slab = b / (t0n * ttn);
     const int64_t rem = b % (t0n * ttn);
-    const int64_t i0 = (rem % t0n) * 32, it = (rem / t0n) * 32;
+    const int64_t i0 = (rem % t0n) * 32, it = (rem / t0n) * 64;
     int64_t so, dof;
     outer_offsets(p, slab, so, dof);
-    // read: consecutive threads along t (unit stride in the source)
-    for (int y = ty; y < 32; y += 8) {
-      const int64_t a = i0 + y, c = it + tx;
-      if (a < e0 && c < et) tile[y][tx] = __ldcs(src + so + a * p.sstr[0] + c);
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // rows y = ty + 8*(j/2), t = it + tx + 32*(j%2)
+      const int64_t a = i0 + ty + 8 * (j >> 1), c = it + tx + 32 * (j & 1);
+      v[j] = (a < e0 && c < et) ? __ldcs(src + so + a * p.sstr[0] + c) : 0.0;
     }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tile[ty + 8 * (j >> 1)][tx + 32 * (j & 1)] = v[j];
     __syncthreads();
-    // write: consecutive threads along dim 0 (unit stride in the destination)
-    for (int y = ty; y < 32; y += 8) {
-      const int64_t a = i0 + tx, c = it + y;
-      if (a < e0 && c < et) __stcs(dst + dof + a + c * p.dstr[p.t], tile[tx][y]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // columns c = it + ty + 8*j, rows a = i0 + tx
+      const int64_t a = i0 + tx, c = it + ty + 8 * j;
+      if (a < e0 && c < et) __stcs(dst + dof + a + c * p.dstr[p.t], tile[tx][ty + 8 * j]);
     }
     __syncthreads();
   }
@@ -149,14 +178,20 @@ int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const d
     return TCB_OK;
   }
   if (p.sstr[0] == 1) {
+    // slabs = every coordinate of dims 2.. (dim 1 is walked inside the block)
     p.outer_n = 0;
-    for (int i = 1; i < p.rank; ++i) p.outer_dim[p.outer_n++] = i;
-    p.rows = total / p.ext[0];
+    for (int i = 2; i < p.rank; ++i) p.outer_dim[p.outer_n++] = i;
+    p.rows = total / (p.ext[0] * (p.rank > 1 ? p.ext[1] : 1));
     bool vec = p.ext[0] % 2 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
                reinterpret_cast<uintptr_t>(dst) % 16 == 0;
     for (int i = 1; i < p.rank && vec; ++i) vec = p.sstr[i] % 2 == 0;
-    const int64_t warps_needed = p.rows;
-    const int blocks = static_cast<int>(std::min<int64_t>((warps_needed + 7) / 8, sms * 16LL));
+    const int64_t L = p.ext[0] / (vec ? 2 : 1);
+    p.t = (L & (L - 1)) == 0 ? __builtin_ctzll(static_cast<unsigned long long>(L)) : -1;
+    // ~4096 vectors (32-64 KB) per block item
+    const int64_t e1 = p.rank > 1 ? p.ext[1] : 1;
+    p.runs_per_chunk = std::max<int64_t>(1, std::min<int64_t>(e1, 4096 / std::max<int64_t>(L, 1)));
+    const int64_t items = p.rows * ((e1 + p.runs_per_chunk - 1) / p.runs_per_chunk);
+    const int blocks = static_cast<int>(std::min<int64_t>(items, sms * 16LL));
     if (vec) perm_runs<true><<<blocks, 256, 0, st.stream>>>(p, src, dst);
     else perm_runs<false><<<blocks, 256, 0, st.stream>>>(p, src, dst);
     TCB_LAUNCHED();
@@ -171,7 +206,7 @@ int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const d
     for (int i = 1; i < p.rank; ++i)
       if (i != t) p.outer_dim[p.outer_n++] = i;
     p.rows = total / (p.ext[0] * p.ext[t]);
-    const int64_t tiles = ((p.ext[0] + 31) / 32) * ((p.ext[t] + 31) / 32) * p.rows;
+    const int64_t tiles = ((p.ext[0] + 31) / 32) * ((p.ext[t] + 63) / 64) * p.rows;
     const int blocks = static_cast<int>(std::min<int64_t>(tiles, sms * 8LL));
     perm_transpose<<<blocks, 256, 0, st.stream>>>(p, src, dst);
     TCB_LAUNCHED();
