@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -145,51 +146,60 @@ __device__ __forceinline__ constexpr int kstep_k(int j, int q) {
 }
 
 // ------------------------------------------------------------- unit decode
+// Index arithmetic below is 32-bit unsigned: the host guarantees units,
+// batch count, M and N (and every group extent) are < 2^31, so no 64-bit
+// division routine is ever called from the kernel.
 struct Unit {
-  int64_t batch;
+  unsigned batch;
   int tm, tn, split;
 };
 
-__device__ __forceinline__ Unit decode_unit(const Params& p, int64_t u) {
+__device__ __forceinline__ Unit decode_unit(const Params& p, int64_t u64) {
+  const unsigned u = static_cast<unsigned>(u64);
+  const unsigned splits = static_cast<unsigned>(p.splits);
   Unit r;
-  r.split = static_cast<int>(u % p.splits);
-  int64_t t = u / p.splits;
-  const int64_t per_batch = static_cast<int64_t>(p.tiles_m) * p.tiles_n;
+  r.split = static_cast<int>(u % splits);
+  const unsigned t = u / splits;
+  const unsigned per_batch = static_cast<unsigned>(p.tiles_m) * static_cast<unsigned>(p.tiles_n);
   r.batch = t / per_batch;
-  int64_t tt = t % per_batch;
+  const unsigned tt = t - r.batch * per_batch;
   // grouped raster: 8 m-tiles share each n-tile sweep (L2 reuse of B)
-  const int64_t group_span = 8LL * p.tiles_n;
-  const int64_t g = tt / group_span;
-  const int first_m = static_cast<int>(g * 8);
-  const int gsize = min(8, p.tiles_m - first_m);
-  const int64_t w = tt % group_span;
+  const unsigned group_span = 8u * static_cast<unsigned>(p.tiles_n);
+  const unsigned g = tt / group_span;
+  const int first_m = static_cast<int>(g * 8u);
+  const unsigned gsize = static_cast<unsigned>(min(8, p.tiles_m - first_m));
+  const unsigned w = tt - g * group_span;
   r.tm = first_m + static_cast<int>(w % gsize);
   r.tn = static_cast<int>(w / gsize);
   return r;
 }
 
-__device__ __forceinline__ void batch_offsets(const Params& p, int64_t b, int64_t& oa,
+__device__ __forceinline__ void batch_offsets(const Params& p, unsigned b, int64_t& oa,
                                               int64_t& ob, int64_t& oc, int* coords) {
   oa = ob = oc = 0;
   for (int i = 0; i < p.nbatch; ++i) {
-    const int64_t e = p.bat_ext[i];
-    const int64_t c = b % e;
-    b /= e;
+    const unsigned e = static_cast<unsigned>(p.bat_ext[i]);
+    const unsigned nb = b / e;
+    const unsigned c = b - nb * e;
+    b = nb;
     coords[i] = static_cast<int>(c);
-    oa += c * p.bat_sa[i];
-    ob += c * p.bat_sb[i];
-    oc += c * p.bat_sc[i];
+    oa += static_cast<int64_t>(c) * p.bat_sa[i];
+    ob += static_cast<int64_t>(c) * p.bat_sb[i];
+    oc += static_cast<int64_t>(c) * p.bat_sc[i];
   }
 }
 
-__device__ __forceinline__ int64_t composite(int64_t idx, int n, const int64_t* ext,
+__device__ __forceinline__ int64_t composite(int64_t idx64, int n, const int64_t* ext,
                                              const int64_t* str) {
+  unsigned idx = static_cast<unsigned>(idx64);
   int64_t off = 0;
   for (int i = 0; i < n - 1; ++i) {
-    off += (idx % ext[i]) * str[i];
-    idx /= ext[i];
+    const unsigned e = static_cast<unsigned>(ext[i]);
+    const unsigned q = idx / e;
+    off += static_cast<int64_t>(idx - q * e) * str[i];
+    idx = q;
   }
-  return off + idx * str[n - 1];
+  return off + static_cast<int64_t>(idx) * str[n - 1];
 }
 
 // ------------------------------------------------------------------ kernel
@@ -280,11 +290,35 @@ __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& 
   }
 }
 
+// Epilogue: thread's 8x4x2 accumulators -> C through the tile's offset tables.
+template <bool BETA>
+__device__ __forceinline__ void store_tile(const double (&acc)[8][4][2], double* Cb,
+                                           const int64_t* s_row, const int64_t (&coff)[4][2],
+                                           const bool (&cok)[4][2], int wm, int r, double alpha,
+                                           double beta) {
+#pragma unroll
+  for (int im = 0; im < 8; ++im) {
+    const int64_t roff = s_row[wm * 64 + im * 8 + r];
+    double* row = Cb + roff;
+    const bool rok = roff >= 0;
+#pragma unroll
+    for (int in = 0; in < 4; ++in)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const bool ok = rok && cok[in][jj];
+        double* dst = row + coff[in][jj];
+        double v = alpha * acc[im][in][jj];
+        if (BETA) v = fma(beta, ok ? *dst : 0.0, v);
+        if (ok) *dst = v;
+      }
+  }
+}
+
 // 384 threads: warpgroup 0 = producer (TMA: one elected thread; cp.async: all
 // 128), warpgroups 1-2 = 8 DMMA consumer warps. setmaxnreg moves registers
 // from the producer (40/thread) to the consumers (232/thread) so the 64-double
 // accumulator tile never spills (a plain 9- or 12-warp CTA caps at 168).
-template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA>
+template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA, bool SPLITK>
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB) {
@@ -422,7 +456,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     double* Cb = p.C + oc;
     const bool use_beta = p.beta != 0.0;
 
-    if (p.splits > 1) {
+    if (SPLITK) {
       // Split-K (cooperative launch: all splits of a tile are co-resident).
       // 1) every split stores its partial tile ([n][m], m contiguous);
       // 2) the splits meet at a per-tile arrival counter;
@@ -496,25 +530,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     consumer_sync();
+    // Branch-free stores (predicated STG): one unrolled copy per beta mode so
+    // the epilogue stays small (it runs once per tile, off the I-cache-hot loop).
     int64_t coff[4][2];
+    bool cok[4][2];
 #pragma unroll
     for (int in = 0; in < 4; ++in)
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) coff[in][jj] = s_col[wn * 32 + in * 8 + 2 * q + jj];
-#pragma unroll
-    for (int im = 0; im < 8; ++im) {
-      const int64_t roff = s_row[wm * 64 + im * 8 + r];
-      if (roff < 0) continue;
-#pragma unroll
-      for (int in = 0; in < 4; ++in)
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          if (coff[in][jj] < 0) continue;
-          double* dst = Cb + roff + coff[in][jj];
-          double v = p.alpha * acc[im][in][jj];
-          if (use_beta) v += p.beta * *dst;
-          *dst = v;
-        }
+      for (int jj = 0; jj < 2; ++jj) {
+        coff[in][jj] = s_col[wn * 32 + in * 8 + 2 * q + jj];
+        cok[in][jj] = coff[in][jj] >= 0;
+      }
+    if (use_beta) {
+      store_tile<true>(acc, Cb, s_row, coff, cok, wm, r, p.alpha, p.beta);
+    } else {
+      store_tile<false>(acc, Cb, s_row, coff, cok, wm, r, p.alpha, p.beta);
     }
   }
 }
@@ -607,13 +637,14 @@ bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t outer, 
 template <bool AK, bool BK_, bool TMA>
 cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap& tb, int grid,
                        cudaStream_t s) {
-  auto kern = dgemm_dmma_kernel<AK, BK_, TMA>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  auto kern = p.splits > 1 ? dgemm_dmma_kernel<AK, BK_, TMA, true>
+                           : dgemm_dmma_kernel<AK, BK_, TMA, false>;
+  static bool attr_set[2] = {false, false};  // per instantiation
+  if (!attr_set[p.splits > 1]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[p.splits > 1] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -690,6 +721,8 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   if (kblocks >= (1LL << 31)) return set_error(TCB_EUNSUPPORTED, "gemm: K too large");
   p.kblocks = static_cast<int>(kblocks);
   const int64_t tiles = batch * p.tiles_m * p.tiles_n;
+  if (d.m >= (1LL << 31) || d.n >= (1LL << 31) || batch >= (1LL << 31) || tiles * 16 >= (1LL << 31))
+    return set_error(TCB_EUNSUPPORTED, "gemm: m, n, batch or tile count above 2^31");
   const int sms = num_sms();
 
   // Split-K when the tile grid leaves most SMs idle (cfg1-type shapes).
