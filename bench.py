@@ -57,8 +57,13 @@ CONFIGS = {
     "cfg5": ("C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=8192,j=8192,k=512,l=512",
              "BASELINE configs[4]: large class-1, i=j=8192, k=l=512"),
 }
-# weak scaling: the label each rank owns a slab of (free label, no collective)
-SHARD_LABEL = {"cfg1": "j", "cfg2": "c", "cfg3": "d", "cfg4": "b", "cfg5": "j"}
+# How a config runs on N ranks (BASELINE.json / SURVEY.md §8e):
+#   weak   each rank evaluates its own full-size slab of a free label (no collective)
+#   shard  strong scaling: the free label is split across ranks (no collective; cfg4 splits b)
+#   ksplit strong scaling: the contracted label is split, partial C reduce-scattered over
+#          NCCL along the outermost output label (cfg5: split l, scatter j)
+MODE = {"cfg1": ("weak", "j"), "cfg2": ("weak", "c"), "cfg3": ("weak", "d"),
+        "cfg4": ("shard", "b"), "cfg5": ("ksplit", "l")}
 L2_BYTES = 126 * 2**20
 
 
@@ -116,10 +121,24 @@ def pinned_array(n: int, dev) -> np.ndarray:
     return a
 
 
-def shard_extents(cfg: str, world: int) -> str:
-    """Per-rank extents: every rank owns a full-size slab of SHARD_LABEL, so
-    per-GPU work is fixed as N grows (weak scaling)."""
-    return CONFIGS[cfg][1]
+def shard_extents(cfg: str, world: int, rank: int) -> str:
+    """Per-rank extents of the contraction this rank evaluates."""
+    from paper_1307_2100_b200 import partition as P
+    mode, label = MODE[cfg]
+    expr, extents, _ = CONFIGS[cfg]
+    if mode == "weak" or world == 1:
+        return extents
+    if mode == "shard":
+        return P.shard_free(expr, extents, label, world, rank).extents
+    return P.shard_contracted(expr, extents, label, world, rank).extents
+
+
+class CudaArray:
+    """Zero-copy view of a device buffer for torch (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3}
 
 
 def cpu_reference(expr: str, extents: str, reps: int, workers: int):
@@ -193,24 +212,59 @@ def main() -> int:
         return run_reference_arm(args, cfg)
 
     rank, world, local = dist_env()
+    # one GPU per rank; ranks beyond the visible GPUs share them round-robin
+    # (only used for single-GPU plumbing tests with TCB_DIST_BACKEND=gloo)
+    import paper_1307_2100_b200 as T
+    ndev = C.c_int(0)
+    T.native.device().tcb_device_count(C.byref(ndev))
+    local = local % max(1, ndev.value)
     torch = None
+    backend = os.environ.get("TCB_DIST_BACKEND", "nccl")  # gloo: plumbing tests on one GPU
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
     import paper_1307_2100_b200 as T
+    from paper_1307_2100_b200 import partition as P
     dev = T.native.device()
     T.check(dev.tcb_init(local), "tcb_init")
-    expr, _, desc = CONFIGS[cfg]
-    extents = shard_extents(cfg, world)
+    expr, full_extents, desc = CONFIGS[cfg]
+    mode, label = MODE[cfg]
+    extents = shard_extents(cfg, world, rank)
+    if world > 1:
+        # one stream for our kernels and NCCL: ordering without host syncs
+        T.check(dev.tcb_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     peak = C.c_double()
     T.check(dev.tcb_fp64_peak(C.byref(peak)), "tcb_fp64_peak")
 
     prep = T.Prepared(expr, extents, device=local)
     info = prep.info()
-    flops = info["flops"]
+    flops = info["flops"]  # this rank's share
+    total_flops = flops * world if mode == "weak" else 2 * int(
+        np.prod([int(v.split("=")[1]) for v in full_extents.split(",")]))
+    collective = None
+    if mode == "ksplit" and world > 1:
+        if backend != "nccl":
+            raise SystemExit("ksplit (cfg5) needs the nccl backend")
+        _, _, optr = prep.device_ptrs()
+        partial = torch.as_tensor(CudaArray(optr, info["output"]), device="cuda")
+        scat = torch.empty(info["output"] // world, dtype=torch.float64, device="cuda")
+
+        def collective():
+            torch.distributed.reduce_scatter_tensor(scat, partial,
+                                                    op=torch.distributed.ReduceOp.SUM)
     L = pinned_array(info["left"], dev)
     R = pinned_array(info["right"], dev)
     O = pinned_array(info["output"], dev)
@@ -224,9 +278,14 @@ def main() -> int:
             torch.cuda.synchronize()
         prep.sync()
 
+    def step():
+        prep.run()
+        if collective is not None:
+            collective()
+
     # ---- device-resident throughput: exactly K steps between two events
     for _ in range(args.warmup):
-        prep.run()
+        step()
     barrier()
     clocks = Clocks(local)
     time.sleep(0.15)
@@ -234,21 +293,17 @@ def main() -> int:
     ms = C.c_float()
     T.check(dev.tcb_timer_start())
     for _ in range(args.steps):
-        prep.run()
+        step()
     T.check(dev.tcb_timer_stop(C.byref(ms)))
     launches = dev.tcb_launch_count()
     clk = clocks.stop()
     barrier()
-    t_ms = float(ms.value)
-    if world > 1:
-        t = torch.tensor([t_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_ms = float(t.item())
+    t_ms = max_over_ranks(float(ms.value))
     step_ms = t_ms / args.steps
-    value = world * flops / (step_ms * 1e-3) / 1e9
+    value = total_flops / (step_ms * 1e-3) / 1e9
 
     # ---- the dominant kernel alone (the contraction launch), events per launch
-    n_kern = max(5, min(args.steps, 50))
+    n_kern = max(3, min(args.steps, 50, int(2000.0 / max(step_ms, 1e-3))))
     prep.run_permutes()
     prep.sync()
     T.check(dev.tcb_timer_start())
@@ -261,7 +316,7 @@ def main() -> int:
     dev.tcb_last_gemm_info(C.byref(gemm_info))
 
     # ---- end to end through the public API with pinned host buffers
-    n_e2e = max(3, min(args.steps, 20))
+    n_e2e = max(3, min(args.steps, 20, int(1000.0 / max(step_ms, 1e-3))))
     prep.upload(L, R)
     prep.run()
     prep.download(O)
@@ -269,26 +324,31 @@ def main() -> int:
     T.check(dev.tcb_timer_start())
     for _ in range(n_e2e):
         prep.upload(L, R)
-        prep.run()
-        prep.download(O)
+        step()
+        if collective is not None:
+            out_view = np.empty(scat.numel())
+            T.check(dev.tcb_d2h(out_view.ctypes.data, scat.data_ptr(), scat.numel() * 8))
+        else:
+            prep.download(O)
     T.check(dev.tcb_timer_stop(C.byref(ms)))
-    e2e_ms = float(ms.value)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * flops / (e2e_ms / n_e2e * 1e-3) / 1e9
+    e2e_ms = max_over_ranks(float(ms.value))
+    e2e_value = total_flops / (e2e_ms / n_e2e * 1e-3) / 1e9
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 6),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if mode == "weak" else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: Tensor::seeded_random uniform[-1,1] (mt19937_64), seeds 1/2 (+2*rank)",
         "config": {
             "workload": desc, "expr": expr, "extents": extents,
             "recipe": info["summary"],
-            "parallelism": "single GPU" if world == 1 else
-                           f"weak: rank r owns {SHARD_LABEL[cfg]}-slab r (no data-path collective)",
+            "parallelism": "single GPU" if world == 1 else {
+                "weak": f"weak: rank r owns its own full-size {label}-slab (no data-path collective)",
+                "shard": f"strong: {label} split {world} ways (no data-path collective)",
+                "ksplit": f"strong: contracted {label} split {world} ways + NCCL reduce-scatter "
+                          f"of partial C over the outermost output label"}[mode],
+            "rank_extents": extents,
             "l2": "inputs larger than L2 per step (A+B+C = %.0f MB > 126 MB)"
                   % ((info['left'] + info['right'] + info['output']) * 8 / 2**20)
                   if (info['left'] + info['right'] + info['output']) * 8 > L2_BYTES else
@@ -296,7 +356,7 @@ def main() -> int:
         },
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": int((info["left"] + info["right"]) * 8),
-                "d2h_bytes_per_step": int(info["output"] * 8),
+                "d2h_bytes_per_step": int(info["output"] * 8 // (world if collective else 1)),
                 "steps": n_e2e, "api": "tcf_upload + tcf_run + tcf_download (include/tcf.h)"},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
                      "peak": round(peak.value, 3), "unit": "TFLOP/s",
