@@ -52,8 +52,18 @@ constexpr int NTHREADS = PTHREADS + CTHREADS;
 constexpr int STAGE_A = BM * BK * 8;   // 16 KB
 constexpr int STAGE_B = BN * BK * 8;   // 16 KB
 constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                           (BM + BN) * 8 /*epilogue offset tables*/;
+constexpr int STAGES_STAGED = 3;       // ring depth when the epilogue is staged
+constexpr int STAGING_BYTES = BM * BN * 8;  // 128 KB: one accumulator tile
+constexpr int TAIL_BYTES = 256 /*barriers*/ + (BM + BN) * 8 /*offset tables*/;
+constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per CTA on sm_100
+// Shared-memory layout: [ring][staging (staged epilogue only)][barriers][tables].
+template <bool STAGED>
+__host__ __device__ constexpr int smem_bytes() {
+  return STAGED ? SMEM_LIMIT
+                : STAGES * STAGE_BYTES + TAIL_BYTES + 1024 /*alignment slack*/;
+}
+static_assert(STAGES_STAGED * STAGE_BYTES + STAGING_BYTES + TAIL_BYTES + 512 <= SMEM_LIMIT,
+              "staged layout must fit with alignment slack");
 
 struct Params {
   const double* A;
@@ -67,6 +77,7 @@ struct Params {
   int nbatch;
   int64_t bat_ext[TCB_MAX_DIMS], bat_sa[TCB_MAX_DIMS], bat_sb[TCB_MAX_DIMS], bat_sc[TCB_MAX_DIMS];
   double alpha, beta;
+  int alpha_ne1, beta_nz;  // alpha != 1, beta != 0 (decided on the host)
   int tiles_m, tiles_n, splits, kblocks;
   int64_t units;
   double* ws;
@@ -322,23 +333,35 @@ template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA, bool SPLITK>
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB) {
+  // Staged epilogue (TMA, no split-K): consumers dump the accumulator tile into
+  // shared memory and go straight on to the next tile's main loop; producer
+  // warps 1-3 apply alpha/beta and write C from there, overlapped with DMMA.
+  constexpr bool STAGED = USE_TMA && !SPLITK;
+  constexpr int NST = STAGED ? STAGES_STAGED : STAGES;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  double* staging = reinterpret_cast<double*>(smem + NST * STAGE_BYTES);
+  unsigned char* tail = smem + NST * STAGE_BYTES + (STAGED ? STAGING_BYTES : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tail);
   const uint32_t s_base = smem_u32(smem);
-  const uint32_t full0 = smem_u32(bars);            // full[s]  = full0 + 8s
-  const uint32_t empty0 = smem_u32(bars + STAGES);  // empty[s] = empty0 + 8s
+  const uint32_t full0 = smem_u32(bars);         // full[s]  = full0 + 8s
+  const uint32_t empty0 = smem_u32(bars + NST);  // empty[s] = empty0 + 8s
+  const uint32_t stg_full = smem_u32(bars + 2 * NST);       // staging holds a tile
+  const uint32_t stg_empty = smem_u32(bars + 2 * NST + 1);  // staging drained
   // per-tile output offsets: composite row(m) / col(n) of the tile, -1 = outside C
-  int64_t* s_row = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + 256);
+  int64_t* s_row = reinterpret_cast<int64_t*>(tail + 256);
   int64_t* s_col = s_row + BM;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    if (tail + TAIL_BYTES > smem_raw + smem_bytes<STAGED>()) __trap();  // alignment slack
+    for (int s = 0; s < NST; ++s) {
       mbar_init(full0 + 8 * s, USE_TMA ? 1 : PTHREADS);
       mbar_init(empty0 + 8 * s, NCW);
     }
+    mbar_init(stg_full, CTHREADS);
+    mbar_init(stg_empty, PTHREADS - 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (USE_TMA) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -348,8 +371,60 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
 
   if (tid < PTHREADS) {
-    // ============================ producer ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    if (STAGED && tid >= 32) {
+      // ========================== storers (warps 1-3) ==========================
+      const int stid = tid - 32;  // 0..95
+      const int swarp = stid >> 5, slane = stid & 31;
+      uint32_t t = 0;
+#pragma unroll 1
+      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++t) {
+        const Unit un = decode_unit(p, u);
+        int bc[TCB_MAX_DIMS];
+        int64_t oa, ob, oc;
+        batch_offsets(p, un.batch, oa, ob, oc, bc);
+        asm volatile("bar.sync 2, 96;" ::: "memory");  // previous tile's tables consumed
+        for (int i = stid; i < BM + BN; i += 96) {
+          if (i < BM) {
+            const int64_t m = static_cast<int64_t>(un.tm) * BM + i;
+            s_row[i] = m < p.M ? composite(m, p.c_nrow, p.c_row_ext, p.c_row_str) : -1;
+          } else {
+            const int64_t n = static_cast<int64_t>(un.tn) * BN + (i - BM);
+            s_col[i - BM] = n < p.N ? composite(n, p.c_ncol, p.c_col_ext, p.c_col_str) : -1;
+          }
+        }
+        asm volatile("bar.sync 2, 96;" ::: "memory");
+        mbar_wait(stg_full, t & 1);
+        double* Cb = p.C + oc;
+        // warp w writes columns n = w, w+3, ...; lanes walk m (coalesced in C).
+        // alpha was applied by the consumers; plain copies keep the FP64 pipe
+        // (shared with DMMA) free unless beta needs a DFMA.
+        const bool use_beta = p.beta_nz != 0;  // host-side flag: no FP64 compare here
+#pragma unroll 1
+        for (int n = swarp; n < BN; n += 3) {
+          const int64_t coff = s_col[n];
+          const uint32_t sw = ((n >> 1) & 1) << 3;
+          double v[BM / 32];
+          int64_t roff[BM / 32];
+#pragma unroll
+          for (int j = 0; j < BM / 32; ++j) {
+            const int m = slane + 32 * j;
+            roff[j] = s_row[m];
+            v[j] = staging[n * BM + (m ^ sw)];
+          }
+          if (coff < 0) continue;
+#pragma unroll
+          for (int j = 0; j < BM / 32; ++j) {
+            if (roff[j] < 0) continue;
+            double* dst = Cb + roff[j] + coff;
+            *dst = use_beta ? fma(p.beta, *dst, v[j]) : v[j];
+          }
+        }
+        mbar_arrive(stg_empty);
+      }
+      return;
+    }
+    // ============================ producer ============================
     if (USE_TMA && tid != 0) return;
     LoadIter li;
     li.u = blockIdx.x;
@@ -357,8 +432,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t g = 0;
 #pragma unroll 1
     while (li.valid) {
-      const uint32_t s = g % STAGES;
-      mbar_wait(empty0 + 8 * s, ((g / STAGES) & 1) ^ 1);
+      const uint32_t s = g % NST;
+      mbar_wait(empty0 + 8 * s, ((g / NST) & 1) ^ 1);
       issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
                                                full0 + 8 * s, tid);
       ++g;
@@ -390,8 +465,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 
   uint32_t gcons = 0;  // k-blocks consumed by this CTA
+  uint32_t tcount = 0;  // tiles finished by this CTA (staging parity)
 #pragma unroll 1
-  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++tcount) {
     const Unit un = decode_unit(p, u);
     const int kb0 = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
     const int kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
@@ -404,8 +480,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 #pragma unroll 1
     for (int kb = kb0; kb < kb1; ++kb) {
-      const uint32_t stage = gcons % STAGES;
-      mbar_wait(full0 + 8 * stage, (gcons / STAGES) & 1);
+      const uint32_t stage = gcons % NST;
+      mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -437,6 +513,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     // ------------------------------ epilogue ------------------------------
+    if constexpr (STAGED) {
+      // hand the tile to the storers: wait until they drained the previous one,
+      // write the raw accumulators ([n][m] with a bank swizzle on m), arrive.
+      if (p.alpha_ne1) {
+#pragma unroll
+        for (int im = 0; im < 8; ++im)
+#pragma unroll
+          for (int in = 0; in < 4; ++in) {
+            acc[im][in][0] *= p.alpha;
+            acc[im][in][1] *= p.alpha;
+          }
+      }
+      mbar_wait(stg_empty, (tcount & 1) ^ 1);
+      const uint32_t sw = (q & 1) << 3;  // ((n >> 1) & 1) << 3 for this thread's columns
+#pragma unroll
+      for (int im = 0; im < 8; ++im)
+#pragma unroll
+        for (int in = 0; in < 4; ++in)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            staging[(wn * 32 + in * 8 + 2 * q + jj) * BM + ((wm * 64 + im * 8 + r) ^ sw)] =
+                acc[im][in][jj];
+      mbar_arrive(stg_full);
+      continue;
+    }
     // Output offsets of this tile's 128 rows and 128 columns, decoded once
     // (one composite index per consumer thread) into shared memory.
     consumer_sync();  // the previous unit's epilogue is done with the tables
@@ -637,19 +738,19 @@ bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t outer, 
 template <bool AK, bool BK_, bool TMA>
 cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap& tb, int grid,
                        cudaStream_t s) {
-  auto kern = p.splits > 1 ? dgemm_dmma_kernel<AK, BK_, TMA, true>
-                           : dgemm_dmma_kernel<AK, BK_, TMA, false>;
+  const bool split = p.splits > 1;
+  auto kern = split ? dgemm_dmma_kernel<AK, BK_, TMA, true> : dgemm_dmma_kernel<AK, BK_, TMA, false>;
+  const int smem = split ? smem_bytes<false>() : smem_bytes<TMA>();
   static bool attr_set[2] = {false, false};  // per instantiation
-  if (!attr_set[p.splits > 1]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
+  if (!attr_set[split]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set[p.splits > 1] = true;
+    attr_set[split] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // split-K CTAs wait on each other
@@ -715,6 +816,8 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   for (int i = 0; i < d.nbatch; ++i) batch *= d.bat_ext[i];
   p.alpha = d.alpha;
   p.beta = d.beta;
+  p.alpha_ne1 = d.alpha != 1.0;
+  p.beta_nz = d.beta != 0.0;
   p.tiles_m = static_cast<int>((d.m + BM - 1) / BM);
   p.tiles_n = static_cast<int>((d.n + BN - 1) / BN);
   const int64_t kblocks = (d.k + BK - 1) / BK;
