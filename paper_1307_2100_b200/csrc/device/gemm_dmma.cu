@@ -575,10 +575,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int jj = 0; jj < 2; ++jj)
             __stcg(part + (wn * 32 + in * 8 + 2 * q + jj) * BM + wm * 64 + im * 8 + r,
                    acc[im][in][jj]);
-      __threadfence();
+      // publish: the CTA barrier orders every thread's partial stores before
+      // thread 0, whose gpu-scope release (cumulative) then announces them
       consumer_sync();
       if (ctid == 0) {
-        atomicAdd(p.counters + tile, 1u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + tile)
+                     : "memory");
         const unsigned target = (p.epoch + 1u) * static_cast<unsigned>(p.splits);
         unsigned seen;
         do {
