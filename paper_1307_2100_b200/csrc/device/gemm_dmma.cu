@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -743,11 +744,16 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
   const bool split = p.splits > 1;
   auto kern = split ? dgemm_dmma_kernel<AK, BK_, TMA, true> : dgemm_dmma_kernel<AK, BK_, TMA, false>;
   const int smem = split ? smem_bytes<false>() : smem_bytes<TMA>();
-  static bool attr_set[2] = {false, false};  // per instantiation
-  if (!attr_set[split]) {
+  // the smem opt-in is a per-device function attribute: remember it per
+  // (instantiation, device) — one bit per device, set once
+  static std::atomic<uint64_t> attr_set[2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set[split].load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set[split] = true;
+    attr_set[split].fetch_or(bit, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);

@@ -1,16 +1,23 @@
 // k4 — level-2/1 recipes: GEMV and DOT (the reference's class-2 and class-1
 // kernels: ReferenceBackend::gemv/dot, src/kernels_reference.cpp:81-120 and
 // :140-149, driven by the executor's GEMV and DOT loops, src/executor.cpp:
-// 181-227). Both are HBM-bound (~8-16 B per FMA), so the design goal is
-// coalescing and enough bytes in flight:
-//   * K-major matrix (k contiguous): one warp per output row and k-chunk,
-//     lanes stream k with 8-byte loads, warp-shuffle tree reduction;
-//   * row-major-in-outer matrix (rows contiguous): 32 rows x 8 threads per
-//     block, coalesced along rows, shared-memory reduction over the k-lanes;
+// 181-227). Both are HBM-bound (~8 B per FMA), so the design goal is
+// coalescing and bytes in flight.
+//
+// Canonical summation order (shared by every kernel below, so results are
+// bit-reproducible and independent of the operand layout — cf. the
+// reference's transpose-equivalence test, tests/test_kernels.cpp:86-116):
+//   K is cut into chunks of `chunk` (a multiple of 64); inside a chunk, k-lane
+//   λ = (k - k0) mod 64 accumulates its terms in increasing k; the 64 lane
+//   sums are paired (2j, 2j+1) and the 32 pairs combined by a fixed xor tree;
+//   chunk results are summed in chunk order by a 256-thread fixed tree.
+//   * K-major matrix (k contiguous): one warp per (row, chunk); lane l owns
+//     k-lanes 2l, 2l+1 and streams them with 16-byte loads, 4 in flight;
+//   * row-contiguous matrix: warps cover 32-64 rows (16-byte loads) or, for
+//     short matrices, several columns per access; each thread owns up to 8
+//     k-lanes (8 loads in flight), combined through shared memory with the
+//     same tree;
 //   * DOT is the one-row case of the K-major kernel.
-// Both kernels sum in the same order (32 k-lanes, fixed combine tree) and long
-// K is split into 32-multiple chunks summed by a second kernel in chunk order,
-// so results are bit-reproducible and independent of the operand layout.
 #include <algorithm>
 
 #include "tcb_internal.cuh"
@@ -30,8 +37,9 @@ struct GvParams {
   int64_t batch;
   double alpha, beta;
   int splits;
-  int64_t chunk;   // k per split
-  double* ws;      // partials [(b*rows + o)*splits + s]
+  int64_t chunk;  // k per split, a multiple of 64
+  bool vec;       // 16-byte loads legal (k-major kernel)
+  double* ws;     // partials [(b*rows + o)*splits + s]
 };
 
 __device__ __forceinline__ void gv_batch(const GvParams& p, int64_t b, int64_t& om, int64_t& ov,
@@ -69,8 +77,8 @@ __device__ __forceinline__ void gv_store(const GvParams& p, int64_t b, int64_t o
   *dst = r;
 }
 
-// one warp per (batch, row, split)
-__global__ void gemv_kmajor(GvParams p) {
+// one warp per (batch, row, split); lane l owns k-lanes 2l and 2l+1
+__global__ void __launch_bounds__(256) gemv_kmajor(GvParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const int64_t items = p.batch * p.rows * p.splits;
@@ -84,27 +92,51 @@ __global__ void gemv_kmajor(GvParams p) {
     const double* mrow = p.M + om + o * p.so;
     const double* vec = p.v + ov;
     const int64_t k0 = s * p.chunk, k1 = min(p.K, k0 + p.chunk);
-    // k-lane l sums k = k0 + l, k0 + l + 32, ... in order; lanes combine in a
-    // fixed xor tree. gemv_omajor reproduces exactly this order.
-    double acc = 0.0;
+    double e0 = 0.0, e1 = 0.0;  // k-lanes 2l, 2l+1
+    if (p.vec) {
+      // k0 is a multiple of 64 and rows/vector 16-byte aligned (checked on host)
+      const int64_t full = k0 + ((k1 - k0) / 64) * 64;
+      int64_t k = k0 + 2 * lane;
 #pragma unroll 4
-    for (int64_t k = k0 + lane; k < k1; k += 32)
-      acc = fma(__ldg(mrow + k * p.sk), __ldg(vec + k * p.sv), acc);
+      for (; k < full; k += 64) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(mrow + k));
+        const double2 x = __ldg(reinterpret_cast<const double2*>(vec + k));
+        e0 = fma(a.x, x.x, e0);
+        e1 = fma(a.y, x.y, e1);
+      }
+      if (k < k1) e0 = fma(__ldcs(mrow + k), __ldg(vec + k), e0);
+      if (k + 1 < k1) e1 = fma(__ldcs(mrow + k + 1), __ldg(vec + k + 1), e1);
+    } else {
+#pragma unroll 4
+      for (int64_t k = k0 + 2 * lane; k < k1; k += 64) {
+        e0 = fma(__ldg(mrow + k * p.sk), __ldg(vec + k * p.sv), e0);
+        if (k + 1 < k1) e1 = fma(__ldg(mrow + (k + 1) * p.sk), __ldg(vec + (k + 1) * p.sv), e1);
+      }
+    }
+    double acc = e0 + e1;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (lane == 0) gv_store(p, b, o, s, acc);
   }
 }
 
-// 32 rows x 8 threads per block; rows are the coalesced direction. Thread ty
-// carries the 4 k-lanes ty, ty+8, ty+16, ty+24 of the 32-lane order used by
-// gemv_kmajor, and the lanes are combined with the same tree, so both layouts
-// give bit-identical results (cf. the reference's transpose-equivalence test,
-// tests/test_kernels.cpp:86-116).
-__global__ void gemv_omajor(GvParams p) {
-  __shared__ double red[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t rblocks = (p.rows + 31) / 32;
+// Row-contiguous matrix, 16 warps per block. A warp covers RL*VR consecutive
+// rows x G = 32/RL consecutive columns, where RL (<= 32) is the number of lanes
+// along rows (fewer than 32 when the matrix has few rows: short-wide matrices
+// still get 256-byte warp accesses). Lane (r, c) owns rows r*VR..r*VR+VR-1
+// (16-byte loads when VR == 2) and, with the warp index ty, the k-lanes
+// c + G*ty + 16G*j of the canonical 64-lane order; the next 64-column step's
+// loads are issued before the current step's FMAs. Lane sums meet in shared
+// memory and are combined with the same tree as gemv_kmajor.
+template <int VR>
+__global__ void __launch_bounds__(512) gemv_omajor(GvParams p, int RL) {
+  __shared__ double red[64][64 + 1];
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int G = 32 / RL;            // columns per warp access
+  const int NJ = 4 / G;             // k-lanes per thread (16 warps; G divides 4)
+  const int r = lane % RL, c = lane / RL;
+  const int rows_per_tile = RL * VR;
+  const int64_t rblocks = (p.rows + rows_per_tile - 1) / rows_per_tile;
   const int64_t items = p.batch * rblocks * p.splits;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int s = static_cast<int>(it % p.splits);
@@ -112,50 +144,100 @@ __global__ void gemv_omajor(GvParams p) {
     const int64_t b = it / (p.splits * rblocks);
     int64_t om, ov, oy;
     gv_batch(p, b, om, ov, oy);
-    const int64_t o = rb * 32 + tx;
+    const int64_t o = rb * rows_per_tile + r * VR;  // first row of this lane
     const int64_t k0 = s * p.chunk, k1 = min(p.K, k0 + p.chunk);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    if (o < p.rows) {
+    double acc[4][VR];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < VR; ++v) acc[j][v] = 0.0;
+    const bool row_ok = o < p.rows;
+    if (row_ok) {
       const double* mcol = p.M + om + o * p.so;
       const double* vec = p.v + ov;
-      for (int64_t kb = k0; kb < k1; kb += 32)
+      // software-pipelined: the next 64-column step's loads are in flight
+      // while the current step's FMAs run (16 loads per thread outstanding)
+      double a[4][VR], x[4];
+      auto load = [&](int64_t kb, double (&aa)[4][VR], double (&xx)[4]) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int64_t k = kb + ty + 8 * j;
-          if (k < k1) acc[j] = fma(__ldg(mcol + k * p.sk), __ldg(vec + k * p.sv), acc[j]);
+          const int64_t k = kb + c + G * (ty + 16 * j);
+          const bool ok = j < NJ && k < k1;
+          xx[j] = ok ? __ldg(vec + k * p.sv) : 0.0;
+          if (VR == 2) {
+            const double2 t = ok ? __ldcs(reinterpret_cast<const double2*>(mcol + k * p.sk))
+                                 : make_double2(0.0, 0.0);
+            aa[j][0] = t.x;
+            aa[j][VR - 1] = t.y;
+          } else {
+            aa[j][0] = ok ? __ldcs(mcol + k * p.sk) : 0.0;
+          }
         }
-    }
+      };
+      load(k0, a, x);
+      for (int64_t kb = k0; kb < k1; kb += 64) {
+        double an[4][VR], xn[4];
+        if (kb + 64 < k1) load(kb + 64, an, xn);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) red[ty + 8 * j][tx] = acc[j];
+        for (int j = 0; j < 4; ++j)
+          if (j < NJ && kb + c + G * (ty + 16 * j) < k1)
+#pragma unroll
+            for (int v = 0; v < VR; ++v) acc[j][v] = fma(a[j][v], x[j], acc[j][v]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          x[j] = xn[j];
+#pragma unroll
+          for (int v = 0; v < VR; ++v) a[j][v] = an[j][v];
+        }
+      }
+    }
+    // red[lambda][row in tile]
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < NJ)
+#pragma unroll
+        for (int v = 0; v < VR; ++v) red[c + G * (ty + 16 * j)][r * VR + v] = acc[j][v];
     __syncthreads();
-    if (ty == 0 && o < p.rows) {
+    for (int rr = threadIdx.x; rr < rows_per_tile; rr += blockDim.x) {
+      const int64_t orow = rb * rows_per_tile + rr;
+      if (orow >= p.rows) continue;
       double l[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) l[i] = red[i][tx];
+      for (int i = 0; i < 32; ++i) l[i] = red[2 * i][rr] + red[2 * i + 1][rr];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
         for (int i = 0; i < off; ++i) l[i] = l[i] + l[i + off];
-      gv_store(p, b, o, s, l[0]);
+      gv_store(p, b, orow, s, l[0]);
     }
     __syncthreads();
   }
 }
 
-__global__ void gemv_finalize(GvParams p) {
+// chunk partials of one output -> y, summed by a fixed 256-thread tree
+__global__ void __launch_bounds__(256) gemv_finalize(GvParams p) {
+  __shared__ double red[256];
   const int64_t n = p.batch * p.rows;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
     const double* part = p.ws + e * p.splits;
     double sum = 0.0;
-    for (int s = 0; s < p.splits; ++s) sum += part[s];
-    const int64_t o = e % p.rows, b = e / p.rows;
-    int64_t om, ov, oy;
-    gv_batch(p, b, om, ov, oy);
-    double* dst = p.y + oy + gv_row(p, o);
-    double r = p.alpha * sum;
-    if (p.beta != 0.0) r += p.beta * *dst;
-    *dst = r;
+    for (int s = threadIdx.x; s < p.splits; s += 256) sum += part[s];
+    red[threadIdx.x] = sum;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+      if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const int64_t o = e % p.rows, b = e / p.rows;
+      int64_t om, ov, oy;
+      gv_batch(p, b, om, ov, oy);
+      double* dst = p.y + oy + gv_row(p, o);
+      double r = p.alpha * red[0];
+      if (p.beta != 0.0) r += p.beta * *dst;
+      *dst = r;
+    }
+    __syncthreads();
   }
 }
 
@@ -207,25 +289,30 @@ int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double
   p.alpha = d.alpha;
   p.beta = d.beta;
   const int sms = num_sms();
-  // the k-contiguous kernel when rows are not unit-stride (or there is one row)
-  const bool kmajor = p.sk == 1 ? (p.so != 1 || p.rows == 1) : (p.so != 1 && p.rows == 1);
-  const bool use_k = kmajor || p.rows == 1;
-  // The k-chunking depends only on the problem (never on which kernel runs)
-  // and chunks are multiples of 32, so the summation order is layout-free.
+  // the k-contiguous kernel when rows are not unit-stride or there is one row
+  const bool use_k = p.rows == 1 || (p.sk == 1 && p.so != 1) || (p.so != 1 && p.sk != 1);
+
+  // Chunking depends only on (batch*rows, K) — never on the kernel — and
+  // chunks are multiples of 64, so the summation order is layout-free.
+  const int64_t rows_total = p.batch * p.rows;
+  const int64_t target = static_cast<int64_t>(sms) * 256;
   int64_t splits = 1;
-  {
-    const int64_t target = static_cast<int64_t>(sms) * 32;
-    const int64_t rows_total = p.batch * p.rows;
-    if (rows_total < target)
-      splits = std::min<int64_t>((target + rows_total - 1) / rows_total,
-                                 std::max<int64_t>(1, d.k / 512));
-  }
-  splits = std::max<int64_t>(1, std::min<int64_t>(splits, 4096));
-  p.chunk = ((d.k + splits - 1) / splits + 31) / 32 * 32;
+  if (rows_total < target)
+    splits = std::min<int64_t>((target + rows_total - 1) / rows_total,
+                               std::max<int64_t>(1, d.k / 1024));
+  splits = std::max<int64_t>(1, std::min<int64_t>(splits, 65536));
+  p.chunk = ((d.k + splits - 1) / splits + 63) / 64 * 64;
   splits = (d.k + p.chunk - 1) / p.chunk;
   p.splits = static_cast<int>(splits);
+
+  // 16-byte loads: unit k-stride, 16-byte aligned row/vector starts
+  bool vec = p.sk == 1 && p.sv == 1 && reinterpret_cast<uintptr_t>(p.M) % 16 == 0 &&
+             reinterpret_cast<uintptr_t>(p.v) % 16 == 0 && (p.rows == 1 || p.so % 2 == 0);
+  for (int i = 0; i < d.nbatch && vec; ++i) vec = p.bat_sm[i] % 2 == 0 && p.bat_sv[i] % 2 == 0;
+  p.vec = vec;
+
   if (splits > 1) {
-    const int64_t need = p.batch * p.rows * splits * 8;
+    const int64_t need = rows_total * splits * 8;
     if (need > st.ws_bytes) {
       if (st.ws) cudaFree(st.ws);
       st.ws = nullptr;
@@ -237,26 +324,35 @@ int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
   int launches = 0;
   if (use_k) {
-    const int64_t warps = p.batch * p.rows * splits;
+    const int64_t warps = rows_total * splits;
     const int blocks = static_cast<int>(std::min<int64_t>((warps + 7) / 8, sms * 32LL));
     gemv_kmajor<<<blocks, 256, 0, st.stream>>>(p);
   } else {
-    const int64_t items = p.batch * ((p.rows + 31) / 32) * splits;
-    const int blocks = static_cast<int>(std::min<int64_t>(items, sms * 16LL));
-    gemv_omajor<<<blocks, 256, 0, st.stream>>>(p);
+    // lanes along rows: fewer than 32 for short matrices (then each warp
+    // access spans several columns); 2 rows per lane when 16-byte loads are legal
+    int RL = 32;
+    while (RL > 1 && RL / 2 >= p.rows) RL /= 2;
+    if (RL < 8) RL = 8;  // G = 32/RL must divide 4
+    bool vr2 = RL == 32 && p.rows >= 64 && p.rows % 2 == 0 && p.so == 1 && p.sk % 2 == 0 &&
+               reinterpret_cast<uintptr_t>(p.M) % 16 == 0;
+    for (int i = 0; i < d.nbatch && vr2; ++i) vr2 = p.bat_sm[i] % 2 == 0;
+    const int per_tile = RL * (vr2 ? 2 : 1);
+    const int64_t items = p.batch * ((p.rows + per_tile - 1) / per_tile) * splits;
+    const int blocks = static_cast<int>(std::min<int64_t>(items, sms * 8LL));
+    if (vr2) gemv_omajor<2><<<blocks, 512, 0, st.stream>>>(p, RL);
+    else gemv_omajor<1><<<blocks, 512, 0, st.stream>>>(p, RL);
   }
   TCB_LAUNCHED();
   ++launches;
   if (splits > 1) {
-    const int64_t n = p.batch * p.rows;
-    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, sms * 8LL));
+    const int blocks = static_cast<int>(std::min<int64_t>(rows_total, sms * 16LL));
     gemv_finalize<<<blocks, 256, 0, st.stream>>>(p);
     TCB_LAUNCHED();
     ++launches;
   }
   st.last_info.path = (d.m == 1 && d.n == 1) ? 3 : 2;
   st.last_info.splits = p.splits;
-  st.last_info.units = p.batch * p.rows * splits;
+  st.last_info.units = rows_total * splits;
   st.last_info.grid = 0;
   st.last_info.launches = launches;
   return TCB_OK;
