@@ -395,6 +395,17 @@ class PreparedContraction {
   void download(double* out);
   void sync();
 
+  /// Host-to-host evaluation with the transfers overlapped with compute: the
+  /// operand carrying the output's outermost label (when that label is also
+  /// its own outermost mode) is uploaded slab by slab on a copy stream while
+  /// earlier slabs are contracted, and output slabs are downloaded on a second
+  /// copy stream as they complete. Needs page-locked host buffers for the
+  /// copies to overlap; otherwise (or when no such label exists) it is
+  /// upload + run + download. `slabs` <= 0 picks ~16 MB slabs (up to 64;
+  /// below 32 MB of streamed data the plain path is used). Returns the slab
+  /// count.
+  int run_streamed(const double* left, const double* right, double* out, int slabs = 0);
+
   const DeviceRecipe& recipe() const { return recipe_; }
   std::int64_t left_elements() const { return nl_; }
   std::int64_t right_elements() const { return nr_; }
@@ -407,11 +418,14 @@ class PreparedContraction {
 
  private:
   DeviceRecipe recipe_;
+  ValidatedContraction v_;
   int device_ = 0;
   std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
   double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;
   double *pl_ = nullptr, *pr_ = nullptr;  // permuted operands (L3)
   std::int64_t launches_ = 0;
+  struct Pipes;
+  std::unique_ptr<Pipes> pipes_;  // streamed path: copy streams + events
 };
 
 }  // namespace tc

@@ -55,6 +55,23 @@ int tcb_d2d(void* dst, const void* src, int64_t bytes);
 int tcb_host_register(void* ptr, int64_t bytes);
 int tcb_host_unregister(void* ptr);
 
+/* Extra streams and events for overlapping copies with compute (the
+ * prepared contraction's streamed host-to-host path). Handles are
+ * cudaStream_t / cudaEvent_t passed as void*. */
+int tcb_stream_create(void** stream);
+int tcb_stream_destroy(void* stream);
+int tcb_event_create(void** event);
+int tcb_event_destroy(void* event);
+int tcb_event_record(void* event, void* stream);
+int tcb_stream_wait_event(void* stream, void* event);
+int tcb_stream_sync(void* stream);
+/* Current stream of this thread (own or caller-set), as void*. */
+void* tcb_current_stream(void);
+/* Asynchronous copy in any direction on `stream` (NULL: current stream). */
+int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* *pinned = 1 when `ptr` is page-locked host memory (registered or allocated). */
+int tcb_host_is_pinned(const void* ptr, int* pinned);
+
 /* ---- the general device recipe ------------------------------------------
  * C[b; m, n] = alpha * sum_k A[b; m, k] * B[b; k, n] + beta * C[b; m, n]
  *   A(m,k) at A + a_off(b) + m*a_sm + k*a_sk

@@ -48,6 +48,11 @@ int tcf_run(void* handle);
 int tcf_run_permutes(void* handle);
 int tcf_run_contraction(void* handle);
 int tcf_download(void* handle, double* out);
+/* Host-to-host evaluation with transfers overlapped with compute
+ * (tc::PreparedContraction::run_streamed); host buffers must be page-locked
+ * (tcb_host_register) for overlap. *slabs_used receives the slab count. */
+int tcf_run_streamed(void* handle, const double* left, const double* right, double* out,
+                     int slabs, int* slabs_used);
 int tcf_sync(void* handle);
 /* info[12]: left, right, output elements; launches of the last run;
  * permuted bytes; m, n, k, batch; flops; number of permutes; device path

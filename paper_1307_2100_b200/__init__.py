@@ -121,6 +121,14 @@ class Prepared:
     def run_contraction(self) -> None:
         self._ok(self._lib.tcf_run_contraction(self._h))
 
+    def run_streamed(self, left: np.ndarray, right: np.ndarray, out: np.ndarray,
+                     slabs: int = 0) -> int:
+        """Host-to-host with H2D/compute/D2H overlapped (pinned buffers)."""
+        used = C.c_int()
+        self._ok(self._lib.tcf_run_streamed(self._h, left.ctypes.data, right.ctypes.data,
+                                            out.ctypes.data, slabs, C.byref(used)))
+        return used.value
+
     def download(self, out: np.ndarray) -> None:
         self._ok(self._lib.tcf_download(self._h, out.ctypes.data))
 

@@ -192,6 +192,88 @@ int tcb_host_unregister(void* ptr) {
   return TCB_OK;
 }
 
+int tcb_stream_create(void** stream) {
+  TCB_TRY_INIT();
+  if (!stream) return set_error(TCB_EINVAL, "tcb_stream_create: null pointer");
+  cudaStream_t s = nullptr;
+  TCB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *stream = s;
+  return TCB_OK;
+}
+
+int tcb_stream_destroy(void* stream) {
+  if (!stream) return TCB_OK;
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+  return TCB_OK;
+}
+
+int tcb_event_create(void** event) {
+  TCB_TRY_INIT();
+  if (!event) return set_error(TCB_EINVAL, "tcb_event_create: null pointer");
+  cudaEvent_t e = nullptr;
+  TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *event = e;
+  return TCB_OK;
+}
+
+int tcb_event_destroy(void* event) {
+  if (!event) return TCB_OK;
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+  return TCB_OK;
+}
+
+static cudaStream_t stream_or_current(void* s) {
+  return s ? static_cast<cudaStream_t>(s) : state().stream;
+}
+
+int tcb_event_record(void* event, void* stream) {
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), stream_or_current(stream)));
+  return TCB_OK;
+}
+
+int tcb_stream_wait_event(void* stream, void* event) {
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaStreamWaitEvent(stream_or_current(stream), static_cast<cudaEvent_t>(event), 0));
+  return TCB_OK;
+}
+
+int tcb_stream_sync(void* stream) {
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaStreamSynchronize(stream_or_current(stream)));
+  return TCB_OK;
+}
+
+void* tcb_current_stream(void) {
+  if (ensure_init() != TCB_OK) return nullptr;
+  return state().stream;
+}
+
+int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  TCB_TRY_INIT();
+  if (bytes < 0) return set_error(TCB_EINVAL, "copy: negative size");
+  if (bytes == 0) return TCB_OK;
+  TCB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
+                           stream_or_current(stream)));
+  return TCB_OK;
+}
+
+int tcb_host_is_pinned(const void* ptr, int* pinned) {
+  TCB_TRY_INIT();
+  if (!pinned) return set_error(TCB_EINVAL, "tcb_host_is_pinned: null pointer");
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *pinned = 0;
+    return TCB_OK;
+  }
+  *pinned = a.type == cudaMemoryTypeHost ? 1 : 0;
+  return TCB_OK;
+}
+
 static int check_desc(const tcb_gemm_desc* d) {
   if (!d) return set_error(TCB_EINVAL, "gemm: null descriptor");
   if (d->m < 0 || d->n < 0 || d->k < 0) return set_error(TCB_EINVAL, "gemm: negative dimension");

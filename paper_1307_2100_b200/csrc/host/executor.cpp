@@ -152,7 +152,7 @@ std::unique_ptr<KernelBackend> make_backend(const std::string& name) {
 // --------------------------------------------------------- PreparedContraction
 
 PreparedContraction::PreparedContraction(const ValidatedContraction& v, int device)
-    : recipe_(lower(v)), device_(device) {
+    : recipe_(lower(v)), v_(v), device_(device) {
   check(tcb_init(device_), "tcb_init");
   nl_ = 1;
   for (int m = 0; m < v.left_rank(); ++m) nl_ *= v.label_at_left_mode(m).extent;
@@ -188,6 +188,7 @@ PreparedContraction::PreparedContraction(const ValidatedContraction& v, int devi
 PreparedContraction::~PreparedContraction() {
   tcb_init(device_);
   tcb_sync();
+  pipes_.reset();
   tcb_free(dl_);
   tcb_free(dr_);
   tcb_free(do_);
@@ -266,6 +267,191 @@ void PreparedContraction::download(double* out) {
 void PreparedContraction::sync() {
   check(tcb_init(device_), "tcb_init");
   check(tcb_sync(), "sync");
+}
+
+namespace {
+
+tcb_gemm_desc desc_of(const DeviceRecipe& r) {
+  tcb_gemm_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.m = r.m;
+  d.n = r.n;
+  d.k = r.k;
+  d.a_sm = r.a_sm;
+  d.a_sk = r.a_sk;
+  d.b_sk = r.b_sk;
+  d.b_sn = r.b_sn;
+  d.c_nrow = static_cast<int32_t>(r.row_ext.size());
+  d.c_ncol = static_cast<int32_t>(r.col_ext.size());
+  for (std::size_t i = 0; i < r.row_ext.size(); ++i) {
+    d.c_row_ext[i] = r.row_ext[i];
+    d.c_row_str[i] = r.row_str[i];
+  }
+  for (std::size_t i = 0; i < r.col_ext.size(); ++i) {
+    d.c_col_ext[i] = r.col_ext[i];
+    d.c_col_str[i] = r.col_str[i];
+  }
+  d.nbatch = static_cast<int32_t>(r.bat_ext.size());
+  for (std::size_t i = 0; i < r.bat_ext.size(); ++i) {
+    d.bat_ext[i] = r.bat_ext[i];
+    d.bat_sa[i] = r.bat_sa[i];
+    d.bat_sb[i] = r.bat_sb[i];
+    d.bat_sc[i] = r.bat_sc[i];
+  }
+  d.alpha = 1.0;
+  d.beta = 0.0;
+  return d;
+}
+
+}  // namespace
+
+// Streams and events of the streamed path, created once per prepared
+// contraction (creating them per call costs more than a small slab).
+struct PreparedContraction::Pipes {
+  void* up = nullptr;
+  void* down = nullptr;
+  std::vector<void*> events;
+  std::size_t next = 0;
+  ~Pipes() {
+    for (void* e : events) tcb_event_destroy(e);
+    tcb_stream_destroy(up);
+    tcb_stream_destroy(down);
+  }
+  void* event() {
+    if (next == events.size()) {
+      void* e = nullptr;
+      check(tcb_event_create(&e), "event");
+      events.push_back(e);
+    }
+    return events[next++];
+  }
+};
+
+int PreparedContraction::run_streamed(const double* left, const double* right, double* out,
+                                      int slabs) {
+  check(tcb_init(device_), "tcb_init");
+  // the stream label: outermost output label, outermost mode of its operand
+  const auto& outs = v_.spec.output.indices;
+  int label = outs.empty() ? -1 : v_.label_index(outs.back().label);
+  bool on_left = false;
+  if (label >= 0) {
+    const LabelInfo& li = v_.labels[static_cast<std::size_t>(label)];
+    on_left = li.left_mode >= 0;
+    const int rank = on_left ? v_.left_rank() : v_.right_rank();
+    const int mode = on_left ? li.left_mode : li.right_mode;
+    if (mode != rank - 1 || li.extent < 2) label = -1;
+  }
+  if (label >= 0) {
+    // a permuted streamed operand must keep the label outermost (contiguous slabs)
+    const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
+    for (const PermuteStep& ps : recipe_.permutes)
+      if (ps.right != on_left &&
+          !(ps.ext.back() == E && ps.src_str.back() * E == (on_left ? nl_ : nr_)))
+        label = -1;
+  }
+  if (label >= 0 && slabs <= 0) {
+    // auto: ~16 MB of streamed operand + output per slab, up to 64 slabs
+    const std::int64_t bytes = ((on_left ? nl_ : nr_) + no_) * 8;
+    slabs = static_cast<int>(std::min<std::int64_t>(64, bytes / (16LL << 20)));
+  }
+  int pinned_l = 0, pinned_r = 0, pinned_o = 0;
+  tcb_host_is_pinned(left, &pinned_l);
+  tcb_host_is_pinned(right, &pinned_r);
+  tcb_host_is_pinned(out, &pinned_o);
+  if (label < 0 || slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
+    upload(left, right);
+    run();
+    download(out);
+    return 1;
+  }
+  const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
+  slabs = static_cast<int>(std::min<std::int64_t>(slabs, E));
+  // per-unit-of-label element counts (the label is outermost, so slabs are
+  // contiguous in the streamed operand and in the output)
+  const std::int64_t s_elems = (on_left ? nl_ : nr_) / E;
+  const std::int64_t o_elems = no_ / E;
+
+  // sub-contraction recipes for the two slab sizes
+  auto sub_recipe = [&](std::int64_t e) {
+    ValidatedContraction sv = v_;
+    sv.labels[static_cast<std::size_t>(label)].extent = e;
+    return lower(sv);
+  };
+  const std::int64_t base = E / slabs, extra = E % slabs;
+  DeviceRecipe rb = sub_recipe(base), rb1 = extra ? sub_recipe(base + 1) : rb;
+
+  if (!pipes_) {
+    pipes_ = std::make_unique<Pipes>();
+    check(tcb_stream_create(&pipes_->up), "stream");
+    check(tcb_stream_create(&pipes_->down), "stream");
+  }
+  Pipes& h = *pipes_;
+  h.next = 0;
+  void* compute = tcb_current_stream();
+  void* up = h.up;
+  void* down = h.down;
+  const std::int64_t before = tcb_launch_count();
+  // the other operand: whole, first; its permutation (if any) once
+  const double* other_host = on_left ? right : left;
+  double* other_dev = on_left ? dr_ : dl_;
+  check(tcb_memcpy_async(other_dev, other_host, (on_left ? nr_ : nl_) * 8, up), "upload");
+  double* stream_dev = on_left ? dl_ : dr_;
+  const double* stream_host = on_left ? left : right;
+  bool other_permuted = false;
+  std::int64_t e0 = 0;
+  for (int s = 0; s < slabs; ++s) {
+    const std::int64_t e = base + (s < extra ? 1 : 0);
+    const DeviceRecipe& r = (s < extra) ? rb1 : rb;
+    check(tcb_memcpy_async(stream_dev + e0 * s_elems, stream_host + e0 * s_elems,
+                           e * s_elems * 8, up),
+          "upload");
+    void* ready = h.event();
+    check(tcb_event_record(ready, up), "event");
+    check(tcb_stream_wait_event(compute, ready), "event");
+    // permutations: the other operand's once, the streamed operand's per slab
+    const double* a = dl_;
+    const double* b = dr_;
+    for (const PermuteStep& ps : r.permutes) {
+      const bool streamed = ps.right != on_left;
+      double* dst = ps.right ? pr_ : pl_;
+      if (streamed) {
+        const std::int64_t off = e0 * (ps.elements / e);
+        check(tcb_permute(static_cast<int>(ps.ext.size()), ps.ext.data(), ps.src_str.data(),
+                          stream_dev + e0 * s_elems, dst + off),
+              "permute");
+      } else if (!other_permuted) {
+        const PermuteStep& full = [&]() -> const PermuteStep& {
+          for (const PermuteStep& q : recipe_.permutes)
+            if (q.right == ps.right) return q;
+          return ps;
+        }();
+        check(tcb_permute(static_cast<int>(full.ext.size()), full.ext.data(),
+                          full.src_str.data(), other_dev, dst),
+              "permute");
+        other_permuted = true;
+      }
+      (ps.right ? b : a) = dst;
+    }
+    // the streamed operand (permuted or not) and C at this slab's offset
+    const std::int64_t s_off = [&]() {
+      for (const PermuteStep& ps : r.permutes)
+        if (ps.right != on_left) return e0 * (ps.elements / e);
+      return e0 * s_elems;
+    }();
+    if (on_left) a += s_off;
+    else b += s_off;
+    tcb_gemm_desc d = desc_of(r);
+    check(tcb_gemm(&d, a, b, do_ + e0 * o_elems), "contraction");
+    void* done = h.event();
+    check(tcb_event_record(done, compute), "event");
+    check(tcb_stream_wait_event(down, done), "event");
+    check(tcb_memcpy_async(out + e0 * o_elems, do_ + e0 * o_elems, e * o_elems * 8, down),
+          "download");
+    e0 += e;
+  }
+  check(tcb_stream_sync(down), "sync");
+  launches_ = tcb_launch_count() - before;
+  return slabs;
 }
 
 // ------------------------------------------------------------------ execute

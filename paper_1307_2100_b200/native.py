@@ -56,6 +56,16 @@ TCB_API = {
     "tcb_d2d": (i32, [vp, vp, i64]),
     "tcb_host_register": (i32, [vp, i64]),
     "tcb_host_unregister": (i32, [vp]),
+    "tcb_stream_create": (i32, [C.POINTER(vp)]),
+    "tcb_stream_destroy": (i32, [vp]),
+    "tcb_event_create": (i32, [C.POINTER(vp)]),
+    "tcb_event_destroy": (i32, [vp]),
+    "tcb_event_record": (i32, [vp, vp]),
+    "tcb_stream_wait_event": (i32, [vp, vp]),
+    "tcb_stream_sync": (i32, [vp]),
+    "tcb_current_stream": (vp, []),
+    "tcb_memcpy_async": (i32, [vp, vp, i64, vp]),
+    "tcb_host_is_pinned": (i32, [vp, C.POINTER(C.c_int)]),
     "tcb_gemm": (i32, [C.POINTER(GemmDesc), vp, vp, vp]),
     "tcb_last_gemm_info": (i32, [C.POINTER(GemmInfo)]),
     "tcb_dgemm": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64]),
@@ -84,6 +94,7 @@ TCF_API = {
     "tcf_run_permutes": (i32, [vp]),
     "tcf_run_contraction": (i32, [vp]),
     "tcf_download": (i32, [vp, vp]),
+    "tcf_run_streamed": (i32, [vp, vp, vp, vp, i32, C.POINTER(C.c_int)]),
     "tcf_sync": (i32, [vp]),
     "tcf_info": (i32, [vp, P_i64, cp, i64]),
     "tcf_device_ptrs": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),

@@ -12,7 +12,7 @@ ROOT = Path(__file__).resolve().parent.parent
 def declared(header: str) -> set[str]:
     text = (ROOT / "include" / header).read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+\**(tc[bf]_\w+)\s*\(",
+    return set(re.findall(r"^\s*(?:int|int64_t|void|const char)\s*\**\s*(tc[bf]_\w+)\s*\(",
                           text, flags=re.M))
 
 

@@ -176,3 +176,32 @@ def test_cfg5_full_size_sampled(dev):
     p.download(got)
     assert np.isfinite(got).all() and del_ok
     assert _sampled_check(e, x, got, L, R, 40, np.random.default_rng(5)) <= TOL
+
+
+@pytest.mark.parametrize("name,e,x", [
+    ("cfg2", "C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]", "a=64,b=48,c=37,k=40"),
+    ("cfg1", "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=96,j=67,k=8,l=12"),
+    ("cfg3", "C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]", "a=16,b=12,c=8,d=13,k=4,l=6"),
+    ("left-streamed", "R[+b,+a] = B[+k,+b] * A[-k,+a]", "a=50,b=30,k=20"),
+])
+def test_streamed_host_path_matches(dev, name, e, x):
+    # tc::PreparedContraction::run_streamed: slabs of the operand carrying the
+    # output's outermost label, H2D / DMMA / D2H overlapped on three streams
+    p = T.Prepared(e, x)
+    inf = p.info()
+    L, R = O.operands(e, x, 1)
+    for a in (L, R):
+        T.check(dev.tcb_host_register(a.ctypes.data, a.nbytes))
+    out = np.zeros(inf["output"])
+    T.check(dev.tcb_host_register(out.ctypes.data, out.nbytes))
+    used = p.run_streamed(L, R, out, slabs=5)
+    assert used == 5, name
+    assert O.max_rel_error(out, O.naive(e, x, L, R)) <= TOL
+    ref = np.empty_like(out)
+    p.upload(L, R)
+    p.run()
+    p.download(ref)
+    assert np.array_equal(out.view(np.uint64), ref.view(np.uint64)) or \
+        O.max_rel_error(out, ref) <= TOL
+    for a in (L, R, out):
+        dev.tcb_host_unregister(a.ctypes.data)
