@@ -36,9 +36,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "tcb_internal.cuh"
 
@@ -84,6 +86,7 @@ struct Params {
   double* ws;
   unsigned* counters;
   unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
+  unsigned long long* trace;  // TCB_TRACE diagnostics: per-CTA phase timestamps (or null)
   // TMA: tensor-map rank and which batch dims each map carries.
   int a_rank, b_rank;
   int a_bdim[3], b_bdim[3];
@@ -127,6 +130,14 @@ __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, 
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
       : "memory");
+}
+// Diagnostics (TCB_TRACE): %globaltimer at phase boundaries, first unit only.
+__device__ __forceinline__ void trace_mark(const Params& p, int slot, bool leader) {
+  if (p.trace != nullptr && leader) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * 8 + slot] = t;
+  }
 }
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(CTHREADS) : "memory");
@@ -467,6 +478,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   uint32_t gcons = 0;  // k-blocks consumed by this CTA
   uint32_t tcount = 0;  // tiles finished by this CTA (staging parity)
+  const bool tl = ctid == 0 && blockIdx.x < p.units;
+  trace_mark(p, 0, tl);
 #pragma unroll 1
   for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++tcount) {
     const Unit un = decode_unit(p, u);
@@ -483,6 +496,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int kb = kb0; kb < kb1; ++kb) {
       const uint32_t stage = gcons % NST;
       mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
+      if (gcons == 0) trace_mark(p, 1, tl);
+      if (gcons == 8) trace_mark(p, 7, tl);
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -514,6 +529,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     // ------------------------------ epilogue ------------------------------
+    if (tcount == 0) trace_mark(p, 2, tl);
     if constexpr (STAGED) {
       // hand the tile to the storers: wait until they drained the previous one,
       // write the raw accumulators ([n][m] with a bank swizzle on m), arrive.
@@ -560,25 +576,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     if (SPLITK) {
       // Split-K (cooperative launch: all splits of a tile are co-resident).
-      // 1) every split stores its partial tile ([n][m], m contiguous);
+      // 1) every split stores its partial tile in fragment order: value pair
+      //    (acc[im][in][0..1]) of consumer thread t at pair index v*256 + t,
+      //    v = im*4 + in — one coalesced 16-byte store per pair;
       // 2) the splits meet at a per-tile arrival counter;
-      // 3) split s reduces elements [s*T/S, (s+1)*T/S) of the tile, summing
-      //    the S partials in split order — bit-reproducible, and the
-      //    reduction is spread over all S CTAs instead of one.
+      // 3) split s reduces pairs [s*P/S, (s+1)*P/S) of the tile, summing the S
+      //    partials in split order — bit-reproducible, spread over all S CTAs.
       const int64_t tile = u / p.splits;
-      double* base = p.ws + tile * p.splits * static_cast<int64_t>(BM * BN);
-      double* part = base + un.split * static_cast<int64_t>(BM * BN);
+      double2* base = reinterpret_cast<double2*>(p.ws) + tile * p.splits * (BM * BN / 2);
+      double2* part = base + un.split * (BM * BN / 2);
 #pragma unroll
       for (int im = 0; im < 8; ++im)
 #pragma unroll
         for (int in = 0; in < 4; ++in)
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-            __stcg(part + (wn * 32 + in * 8 + 2 * q + jj) * BM + wm * 64 + im * 8 + r,
-                   acc[im][in][jj]);
+          __stcg(part + (im * 4 + in) * CTHREADS + ctid,
+                 make_double2(acc[im][in][0], acc[im][in][1]));
       // publish: the CTA barrier orders every thread's partial stores before
       // thread 0, whose gpu-scope release (cumulative) then announces them
       consumer_sync();
+      if (tcount == 0) trace_mark(p, 3, tl);
       if (ctid == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + tile)
                      : "memory");
@@ -587,49 +603,66 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.counters + tile)
                        : "memory");
-          if (seen < target) __nanosleep(64);
+          if (seen < target) __nanosleep(32);
         } while (seen < target);
       }
       consumer_sync();
-      const int e0 = (BM * BN) * un.split / p.splits;
-      const int e1 = (BM * BN) * (un.split + 1) / p.splits;
-      // Each thread owns up to RED_ELEMS elements of the slice and issues all
-      // their S partial loads before summing (one L2 round trip, not S).
-      constexpr int RED_ELEMS = 8;
+      if (tcount == 0) trace_mark(p, 4, tl);
+      constexpr int PAIRS = BM * BN / 2;
+      const int p0 = PAIRS * un.split / p.splits;
+      const int p1 = PAIRS * (un.split + 1) / p.splits;
+      // Each thread owns up to RED pairs of the slice and issues all their S
+      // partial loads before summing (one L2 round trip, not S).
+      constexpr int RED = 4;
 #pragma unroll 1
-      for (int eb = e0 + ctid; eb < e1; eb += CTHREADS * RED_ELEMS) {
-        double sum[RED_ELEMS];
+      for (int pb = p0 + ctid; pb < p1; pb += CTHREADS * RED) {
+        double2 sum[RED];
 #pragma unroll
-        for (int i = 0; i < RED_ELEMS; ++i) sum[i] = 0.0;
+        for (int i = 0; i < RED; ++i) sum[i] = make_double2(0.0, 0.0);
 #pragma unroll 1
         for (int sp0 = 0; sp0 < p.splits; sp0 += 4) {
-          double v[4][RED_ELEMS];
+          double2 v[4][RED];
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
-            for (int i = 0; i < RED_ELEMS; ++i) {
-              const int e = eb + i * CTHREADS;
-              v[j][i] = (sp0 + j < p.splits && e < e1)
-                            ? __ldcg(base + (sp0 + j) * (BM * BN) + e) : 0.0;
+            for (int i = 0; i < RED; ++i) {
+              const int pi = pb + i * CTHREADS;
+              v[j][i] = (sp0 + j < p.splits && pi < p1)
+                            ? __ldcg(base + (sp0 + j) * PAIRS + pi) : make_double2(0.0, 0.0);
             }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
-            for (int i = 0; i < RED_ELEMS; ++i)
-              if (sp0 + j < p.splits) sum[i] += v[j][i];  // split order 0..S-1
+            for (int i = 0; i < RED; ++i)
+              if (sp0 + j < p.splits) {  // split order 0..S-1
+                sum[i].x += v[j][i].x;
+                sum[i].y += v[j][i].y;
+              }
         }
 #pragma unroll
-        for (int i = 0; i < RED_ELEMS; ++i) {
-          const int e = eb + i * CTHREADS;
-          if (e >= e1) continue;
-          const int64_t roff = s_row[e & (BM - 1)], coff = s_col[e >> 7];
-          if (roff < 0 || coff < 0) continue;
-          double* dst = Cb + roff + coff;
-          double vv = p.alpha * sum[i];
-          if (use_beta) vv += p.beta * *dst;
-          *dst = vv;
+        for (int i = 0; i < RED; ++i) {
+          const int pi = pb + i * CTHREADS;
+          if (pi >= p1) continue;
+          // pair index -> (m, n): v = pi / 256 (im = v/4, in = v%4), thread t = pi % 256
+          const int v = pi >> 8, t = pi & 255;
+          const int tw = t >> 5, tl2 = t & 31;
+          const int m = (tw & 1) * 64 + (v >> 2) * 8 + (tl2 >> 2);
+          const int n = (tw >> 1) * 32 + (v & 3) * 8 + 2 * (tl2 & 3);
+          const int64_t roff = s_row[m];
+          if (roff < 0) continue;
+          const double sv[2] = {sum[i].x, sum[i].y};
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int64_t coff = s_col[n + jj];
+            if (coff < 0) continue;
+            double* dst = Cb + roff + coff;
+            double vv = p.alpha * sv[jj];
+            if (use_beta) vv += p.beta * *dst;
+            *dst = vv;
+          }
         }
       }
+      if (tcount == 0) trace_mark(p, 5, tl);
       continue;
     }
 
@@ -651,6 +684,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       store_tile<false>(acc, Cb, s_row, coff, cok, wm, r, p.alpha, p.beta);
     }
   }
+  trace_mark(p, 6, tl);
 }
 
 // beta-only update (alpha == 0 or K == 0): C <- beta*C, or 0 when beta == 0
@@ -888,6 +922,14 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   if (tma && !b_k && p.b_so != 1 && d.n > 1) tma = false;
 
   const int grid = static_cast<int>(std::min<int64_t>(p.units, sms));
+  // TCB_TRACE=<file>: append per-CTA phase timestamps of this launch (diagnostics)
+  static const char* trace_path = getenv("TCB_TRACE");
+  unsigned long long* trace = nullptr;
+  if (trace_path) {
+    TCB_CUDA(cudaMalloc(&trace, grid * 8 * sizeof(unsigned long long)));
+    TCB_CUDA(cudaMemsetAsync(trace, 0, grid * 8 * sizeof(unsigned long long), st.stream));
+  }
+  p.trace = trace;
   cudaError_t e;
   if (tma) {
     if (a_k && b_k) e = launch_one<true, true, true>(p, ta, tb, grid, st.stream);
@@ -905,6 +947,20 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     return cuda_fail(e, "dgemm_dmma launch");
   }
   ++st.launches;
+  if (trace) {
+    std::vector<unsigned long long> h(static_cast<size_t>(grid) * 8);
+    TCB_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st.stream));
+    TCB_CUDA(cudaStreamSynchronize(st.stream));
+    cudaFree(trace);
+    if (FILE* f = fopen(trace_path, "a")) {
+      fprintf(f, "{\"m\":%lld,\"n\":%lld,\"k\":%lld,\"splits\":%d,\"grid\":%d,\"t\":[",
+              static_cast<long long>(d.m), static_cast<long long>(d.n),
+              static_cast<long long>(d.k), splits, grid);
+      for (size_t i = 0; i < h.size(); ++i) fprintf(f, "%s%llu", i ? "," : "", h[i]);
+      fprintf(f, "]}\n");
+      fclose(f);
+    }
+  }
   if (splits > 1) {
     ++st.epoch;  // the counters of these tiles now hold epoch*splits
     st.last_splits = splits;
