@@ -366,11 +366,18 @@ struct DeviceRecipe {
   std::int64_t a_sm = 1, a_sk = 1, b_sk = 1, b_sn = 1;
   std::vector<std::int64_t> row_ext, row_str, col_ext, col_str;
   std::vector<std::int64_t> bat_ext, bat_sa, bat_sb, bat_sc;
-  std::string layout;  // "L1" in place, "L2" batched, "L3" permuted
+  // "L4" only: m, n, k as composites of operand dimensions read in place
+  // (sub-index extents first fastest, per-operand strides; tcb_gemm_desc g_*)
+  std::vector<std::int64_t> gm_ext, gm_sa, gn_ext, gn_sb, gk_ext, gk_sa, gk_sb;
+  // "L1" in place, "L2" batched, "L3" permuted, "L4" in-place index groups
+  std::string layout;
   std::string summary() const;
 };
 
-DeviceRecipe lower(const ValidatedContraction& v);
+/// Lower a validated contraction to one device recipe. `index_groups` allows
+/// the L4 form (operands read in place through composite tensor-map boxes)
+/// where L3 would otherwise permute an operand.
+DeviceRecipe lower(const ValidatedContraction& v, bool index_groups = true);
 
 /// A contraction lowered once and bound to device buffers, for repeated
 /// execution without host round trips (no reference counterpart; bench.py
@@ -419,6 +426,7 @@ class PreparedContraction {
  private:
   DeviceRecipe recipe_;
   ValidatedContraction v_;
+  bool groups_ok_ = true;  // L4 allowed (cleared if the device refuses it)
   int device_ = 0;
   std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
   double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;

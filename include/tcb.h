@@ -93,6 +93,19 @@ typedef struct tcb_gemm_desc {
   int64_t bat_ext[TCB_MAX_DIMS];
   int64_t bat_sa[TCB_MAX_DIMS], bat_sb[TCB_MAX_DIMS], bat_sc[TCB_MAX_DIMS];
   double alpha, beta;
+  /* Optional operand index groups (all 0: the single strides a_sm, a_sk,
+   * b_sk, b_sn above). With g_m, g_n, g_k > 0, m, n and k are composite
+   * indices over that many sub-indices (first fastest) of extents m_ext,
+   * n_ext, k_ext (products m, n, k), and the operands are read in place:
+   *   A(m,k) at A + a_off(b) + sum_i m_i*a_m_str[i] + sum_j k_j*a_k_str[j]
+   *   B(k,n) at B + b_off(b) + sum_j k_j*b_k_str[j] + sum_i n_i*b_n_str[i].
+   * This removes the operand permutation of COPY+GEMM (class 3 of the
+   * paper's taxonomy) where the groups fit the operand tensor maps; see
+   * tcb_gemm_check. */
+  int32_t g_m, g_n, g_k;
+  int64_t m_ext[TCB_MAX_DIMS], a_m_str[TCB_MAX_DIMS];
+  int64_t n_ext[TCB_MAX_DIMS], b_n_str[TCB_MAX_DIMS];
+  int64_t k_ext[TCB_MAX_DIMS], a_k_str[TCB_MAX_DIMS], b_k_str[TCB_MAX_DIMS];
 } tcb_gemm_desc;
 
 /* Execution report for the last tcb_gemm on this thread. */
@@ -106,6 +119,11 @@ typedef struct tcb_gemm_info {
 
 int tcb_gemm(const tcb_gemm_desc* d, const double* A, const double* B, double* C);
 int tcb_last_gemm_info(tcb_gemm_info* info);
+/* TCB_OK when tcb_gemm can execute `d` for 16-byte aligned operands (only
+ * descriptors with index groups can be refused: the groups must map onto the
+ * tensor-map boxes of the DMMA kernel); TCB_EUNSUPPORTED with the reason
+ * otherwise. Needs an initialised device (the encoder is a driver call). */
+int tcb_gemm_check(const tcb_gemm_desc* d);
 
 /* BLAS-semantics GEMM on device buffers: C <- alpha*op(A)*op(B) + beta*C.
  * Replaces KernelBackend::gemm (include/tc/kernels.hpp:20-23,

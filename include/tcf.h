@@ -33,7 +33,9 @@ int tcf_execute(const char* expr, int positional, const char* extents, uint64_t 
                 int64_t errcap);
 
 /* The device recipe (lowering) of a contraction, without touching a device:
- * "L1|L2|L3 gemm m=.. n=.. k=.. a(sm,sk) b(sk,sn) batch=[..] permutes=N". */
+ * "L1|L2|L3 gemm m=.. n=.. k=.. a(sm,sk) b(sk,sn) batch=[..] permutes=N", or
+ * "L4 gemm m=.. n=.. k=.. m[ext:str,..] n[..] k[ext:str_a/str_b,..] ..." for
+ * in-place index groups (TC_INDEX_GROUPS=0 in the environment disables L4). */
 int tcf_lower(const char* expr, int positional, const char* extents, char* buf, int64_t cap);
 
 /* Fill `out` with Tensor::seeded_random's stream (src/tensor.cpp:54-62). */

@@ -287,7 +287,27 @@ static int check_desc(const tcb_gemm_desc* d) {
     return set_error(TCB_EINVAL, "gemm: output index groups do not cover m x n");
   for (int i = 0; i < d->nbatch; ++i)
     if (d->bat_ext[i] <= 0) return set_error(TCB_EINVAL, "gemm: batch extent must be positive");
+  if (d->g_m != 0 || d->g_n != 0 || d->g_k != 0) {
+    if (d->g_m < 1 || d->g_m > TCB_MAX_DIMS || d->g_n < 1 || d->g_n > TCB_MAX_DIMS ||
+        d->g_k < 1 || d->g_k > TCB_MAX_DIMS)
+      return set_error(TCB_EUNSUPPORTED, "gemm: operand index-group rank outside [1, 6]");
+    int64_t pm = 1, pn = 1, pk = 1;
+    for (int i = 0; i < d->g_m; ++i) pm *= d->m_ext[i];
+    for (int i = 0; i < d->g_n; ++i) pn *= d->n_ext[i];
+    for (int i = 0; i < d->g_k; ++i) pk *= d->k_ext[i];
+    if (pm != d->m || pn != d->n || pk != d->k)
+      return set_error(TCB_EINVAL, "gemm: operand index groups do not cover m, n, k");
+    if (d->m < 2 || d->n < 2)
+      return set_error(TCB_EUNSUPPORTED, "gemm: operand index groups need m, n >= 2");
+  }
   return TCB_OK;
+}
+
+int tcb_gemm_check(const tcb_gemm_desc* d) {
+  TCB_TRY_INIT();
+  const int rc = check_desc(d);
+  if (rc != TCB_OK) return rc;
+  return check_gemm_groups(*d);
 }
 
 int tcb_gemm(const tcb_gemm_desc* d, const double* A, const double* B, double* C) {

@@ -68,6 +68,17 @@ __host__ __device__ constexpr int smem_bytes() {
 static_assert(STAGES_STAGED * STAGE_BYTES + STAGING_BYTES + TAIL_BYTES + 512 <= SMEM_LIMIT,
               "staged layout must fit with alignment slack");
 
+// How the producer derives the 5 coordinates of an operand tensor map from
+// the (outer index, k index, batch index) of a box origin: dimension d reads
+// source src[d] (0 outer, 1 k, 2 batch, 3 constant 0) and takes
+// (value / div[d]) % mod[d] (mod 0: no modulus). Composite index groups —
+// several tensor dimensions forming one GEMM index — are thereby read in
+// place, with no permutation pass.
+struct MapProg {
+  unsigned div[5], mod[5];
+  int src[5];
+};
+
 struct Params {
   const double* A;
   const double* B;
@@ -87,9 +98,8 @@ struct Params {
   unsigned* counters;
   unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
   unsigned long long* trace;  // TCB_TRACE diagnostics: per-CTA phase timestamps (or null)
-  // TMA: tensor-map rank and which batch dims each map carries.
-  int a_rank, b_rank;
-  int a_bdim[3], b_bdim[3];
+  // TMA coordinate programs of the A and B tensor maps (see MapProg)
+  MapProg pa, pb;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -234,33 +244,45 @@ struct LoadIter {
   int kb, kb1;
   int m0, n0;            // tile origin (TMA coordinates are int32)
   int64_t oa, ob;        // batch offsets (cp.async path)
-  int ca[3], cb[3];      // batch coordinates of the A / B tensor maps
+  unsigned batch;        // batch index (TMA path: decoded by the map programs)
   bool valid;
 
+  template <bool USE_TMA>
   __device__ __forceinline__ void start_unit(const Params& p) {
     valid = u < p.units;
     if (!valid) return;
     const Unit un = decode_unit(p, u);
-    int bc[TCB_MAX_DIMS];
-    int64_t oc;
-    batch_offsets(p, un.batch, oa, ob, oc, bc);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      ca[i] = i < p.a_rank - 2 ? bc[p.a_bdim[i]] : 0;
-      cb[i] = i < p.b_rank - 2 ? bc[p.b_bdim[i]] : 0;
+    batch = un.batch;
+    if (!USE_TMA) {
+      int bc[TCB_MAX_DIMS];
+      int64_t oc;
+      batch_offsets(p, un.batch, oa, ob, oc, bc);
     }
     kb = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
     kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
     m0 = un.tm * BM;
     n0 = un.tn * BN;
   }
+  template <bool USE_TMA>
   __device__ __forceinline__ void advance(const Params& p) {
     if (++kb == kb1) {
       u += gridDim.x;
-      start_unit(p);
+      start_unit<USE_TMA>(p);
     }
   }
 };
+
+__device__ __forceinline__ void map_coords(const MapProg& g, unsigned o, unsigned k, unsigned b,
+                                           int (&c)[5]) {
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    const int s = g.src[d];
+    unsigned v = s == 0 ? o : (s == 1 ? k : (s == 2 ? b : 0u));
+    if (g.div[d] != 1u) v /= g.div[d];
+    if (g.mod[d] != 0u) v %= g.mod[d];
+    c[d] = static_cast<int>(v);
+  }
+}
 
 // Issue one k-block of both operands into a stage. TMA: one thread, 5-D maps
 // (lead, other, 3 batch dims). cp.async: the 128 producer threads.
@@ -272,19 +294,17 @@ __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& 
   const uint32_t sB = sA + STAGE_A;
   if (USE_TMA) {
     mbar_expect_tx(full, STAGE_BYTES);
-    if (A_KMAJOR) {
-      tma_load5(sA, &tmA, full, k0, li.m0, li.ca[0], li.ca[1], li.ca[2]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < BM / 16; ++i)
-        tma_load5(sA + i * 2048, &tmA, full, li.m0 + 16 * i, k0, li.ca[0], li.ca[1], li.ca[2]);
+    int c[5];
+    // K-major: one 16(k) x 128(outer) box; MN-major: 8 boxes of 16 x 16
+#pragma unroll 1
+    for (int i = 0; i < (A_KMAJOR ? 1 : BM / 16); ++i) {
+      map_coords(p.pa, li.m0 + 16 * i, k0, li.batch, c);
+      tma_load5(sA + i * 2048, &tmA, full, c[0], c[1], c[2], c[3], c[4]);
     }
-    if (B_KMAJOR) {
-      tma_load5(sB, &tmB, full, k0, li.n0, li.cb[0], li.cb[1], li.cb[2]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < BN / 16; ++i)
-        tma_load5(sB + i * 2048, &tmB, full, li.n0 + 16 * i, k0, li.cb[0], li.cb[1], li.cb[2]);
+#pragma unroll 1
+    for (int i = 0; i < (B_KMAJOR ? 1 : BN / 16); ++i) {
+      map_coords(p.pb, li.n0 + 16 * i, k0, li.batch, c);
+      tma_load5(sB + i * 2048, &tmB, full, c[0], c[1], c[2], c[3], c[4]);
     }
   } else {
     const double* Ab = p.A + li.oa;
@@ -440,7 +460,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (USE_TMA && tid != 0) return;
     LoadIter li;
     li.u = blockIdx.x;
-    li.start_unit(p);
+    li.template start_unit<USE_TMA>(p);
     uint32_t g = 0;
 #pragma unroll 1
     while (li.valid) {
@@ -449,7 +469,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
                                                full0 + 8 * s, tid);
       ++g;
-      li.advance(p);
+      li.template advance<USE_TMA>(p);
     }
     if (!USE_TMA) asm volatile("cp.async.wait_all;" ::: "memory");
     return;
@@ -722,54 +742,144 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Build the tensor map of one operand: dims (outer, k) or (k, outer) plus the
-// batch dims whose stride is non-zero. Returns false when TMA cannot describe
-// the operand (alignment, strides, rank) — the caller then uses cp.async.
-bool make_map(CUtensorMap* map, const double* base, bool kmajor, int64_t outer, int64_t K,
-              int64_t s_outer, int64_t s_k, const tcb_gemm_desc& d, const int64_t* bstr,
-              int* rank, int* bdim) {
+// One GEMM index of one operand as a composite of tensor dimensions (first
+// fastest): a single (extent, stride) for plain descriptors.
+struct Group {
+  int n = 0;
+  int64_t ext[TCB_MAX_DIMS] = {};
+  int64_t str[TCB_MAX_DIMS] = {};
+  void one(int64_t e, int64_t st) {
+    n = 1;
+    ext[0] = e;
+    str[0] = st;
+  }
+  void many(int g, const int64_t* e, const int64_t* st) {
+    n = g;
+    for (int i = 0; i < g; ++i) {
+      ext[i] = e[i];
+      str[i] = st[i];
+    }
+  }
+};
+
+// The operand groups of a descriptor.
+struct OperandGroups {
+  Group am, ak, bk, bn;
+};
+OperandGroups groups_of(const tcb_gemm_desc& d) {
+  OperandGroups g;
+  if (d.g_m > 0) g.am.many(d.g_m, d.m_ext, d.a_m_str);
+  else g.am.one(d.m, d.a_sm);
+  if (d.g_n > 0) g.bn.many(d.g_n, d.n_ext, d.b_n_str);
+  else g.bn.one(d.n, d.b_sn);
+  if (d.g_k > 0) {
+    g.ak.many(d.g_k, d.k_ext, d.a_k_str);
+    g.bk.many(d.g_k, d.k_ext, d.b_k_str);
+  } else {
+    g.ak.one(d.k, d.a_sk);
+    g.bk.one(d.k, d.b_sk);
+  }
+  return g;
+}
+bool has_groups(const tcb_gemm_desc& d) { return d.g_m > 0 || d.g_n > 0 || d.g_k > 0; }
+
+// Build the tensor map of one operand and its coordinate program. Dimension
+// order: [lead inner: the unit-stride sub-index, box 16] [other inner: box 16
+// (MN-major) or 128 (K-major), spilling into the next sub-index when the inner
+// extent divides 128] [remaining sub-indices, box 1] [batch dims with a
+// non-zero stride, box 1]. Box rows never straddle a sub-index boundary: inner
+// extents of multi-dimension groups must be multiples of the box (or, K-major,
+// divide 128). Returns false with `why` set when TMA cannot describe the
+// operand; plain descriptors then fall back to cp.async.
+bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
+              const Group& outer, const Group& kg, const tcb_gemm_desc& d, const int64_t* bstr,
+              const char** why) {
+  auto fail = [&](const char* w) {
+    *why = w;
+    return false;
+  };
   auto fn = encode_fn();
-  if (!fn) return false;
-  if (reinterpret_cast<uintptr_t>(base) % 16) return false;
-  cuuint64_t dims[5], strides[4];
-  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
-  const int64_t lead_ext = kmajor ? K : outer;
-  const int64_t other_ext = kmajor ? outer : K;
-  const int64_t other_str = kmajor ? s_outer : s_k;
-  if ((kmajor ? s_k : s_outer) != 1 && lead_ext > 1) return false;
-  if (lead_ext >= (1LL << 31) || other_ext >= (1LL << 31)) return false;
-  dims[0] = static_cast<cuuint64_t>(lead_ext);
-  dims[1] = static_cast<cuuint64_t>(other_ext);
-  box[0] = 16;
-  box[1] = kmajor ? 128 : 16;
-  int64_t os = other_ext > 1 ? other_str : 2;  // extent-1 dims: any legal stride
-  if (os <= 0 || os % 2 || os * 8 >= (1LL << 40)) return false;
-  strides[0] = static_cast<cuuint64_t>(os * 8);
-  int r = 2;
-  for (int i = 0; i < d.nbatch; ++i) {
-    if (bstr[i] == 0 || d.bat_ext[i] == 1) continue;
-    if (r == 5) return false;
-    if (bstr[i] < 0 || bstr[i] % 2 || bstr[i] * 8 >= (1LL << 40)) return false;
-    if (d.bat_ext[i] >= (1LL << 31)) return false;
-    dims[r] = static_cast<cuuint64_t>(d.bat_ext[i]);
-    strides[r - 1] = static_cast<cuuint64_t>(bstr[i] * 8);
-    box[r] = 1;
-    bdim[r - 2] = i;
+  if (!fn) return fail("tensor-map encoder unavailable");
+  if (reinterpret_cast<uintptr_t>(base) % 16) return fail("operand not 16-byte aligned");
+  struct Dim {
+    int64_t ext, str;
+    uint32_t box;
+    int src;
+    int64_t div, mod;
+  };
+  Dim dims[16];
+  int r = 0;
+  auto push = [&](int64_t ext, int64_t str, uint32_t box, int src, int64_t div, int64_t mod) {
+    if (r < 16) dims[r] = Dim{ext, str, box, src, div, mod};
     ++r;
+  };
+  const Group& lead = kmajor ? kg : outer;
+  const Group& other = kmajor ? outer : kg;
+  const int lsrc = kmajor ? 1 : 0, osrc = kmajor ? 0 : 1;
+  if (lead.str[0] != 1 && lead.ext[0] > 1) return fail("no unit-stride inner index");
+  if (lead.n > 1 && lead.ext[0] % 16) return fail("inner extent of a unit-stride group not a multiple of 16");
+  push(lead.ext[0], 1, 16, lsrc, 1, lead.n > 1 ? lead.ext[0] : 0);
+  const uint32_t obox = kmajor ? BN : 16;
+  const int64_t e0 = other.ext[0];
+  int rest = 1;
+  int64_t div = e0;
+  if (other.n > 1 && e0 % obox) {
+    if (!kmajor || obox % e0) return fail("inner extent of a strided group does not tile the box");
+    const int64_t e1 = other.ext[1], b1 = obox / e0;
+    if (other.n > 2 && e1 % b1) return fail("second extent of a strided group does not tile the box");
+    push(e0, other.str[0], static_cast<uint32_t>(e0), osrc, 1, e0);
+    push(e1, other.str[1], static_cast<uint32_t>(b1), osrc, e0, other.n > 2 ? e1 : 0);
+    rest = 2;
+    div = e0 * e1;
+  } else {
+    push(e0, other.str[0], obox, osrc, 1, other.n > 1 ? e0 : 0);
   }
-  *rank = r;
-  // Always encode 5 dims (unused ones: extent 1) so the kernel issues a single
-  // instruction form (cp.async.bulk.tensor.5d) whatever the batch rank.
-  for (; r < 5; ++r) {
-    dims[r] = 1;
-    strides[r - 1] = strides[r - 2];
-    box[r] = 1;
+  for (int j = rest; j < other.n; ++j) {
+    push(other.ext[j], other.str[j], 1, osrc, div, j + 1 < other.n ? other.ext[j] : 0);
+    div *= other.ext[j];
   }
+  div = lead.ext[0];
+  for (int j = 1; j < lead.n; ++j) {
+    push(lead.ext[j], lead.str[j], 1, lsrc, div, j + 1 < lead.n ? lead.ext[j] : 0);
+    div *= lead.ext[j];
+  }
+  div = 1;
+  for (int i = 0; i < d.nbatch; ++i) {
+    if (bstr[i] != 0 && d.bat_ext[i] > 1) push(d.bat_ext[i], bstr[i], 1, 2, div, d.bat_ext[i]);
+    div *= d.bat_ext[i];
+  }
+  if (r > 5) return fail("more than 5 tensor-map dimensions");
+  cuuint64_t gdim[5], gstr[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    const Dim x = i < r ? dims[i] : Dim{1, 2, 1, 3, 1, 0};
+    if (x.ext >= (1LL << 31) || x.div >= (1LL << 32) || x.mod >= (1LL << 32))
+      return fail("extent above 2^31");
+    gdim[i] = static_cast<cuuint64_t>(x.ext);
+    box[i] = x.box;
+    if (i > 0) {
+      const int64_t st = x.ext > 1 ? x.str : 2;  // extent-1 dims: any legal stride
+      if (st <= 0 || st % 2 || st * 8 >= (1LL << 40)) return fail("stride not a positive multiple of 16 bytes");
+      gstr[i - 1] = static_cast<cuuint64_t>(st * 8);
+    }
+    prog->src[i] = x.src;
+    prog->div[i] = static_cast<unsigned>(x.div);
+    prog->mod[i] = static_cast<unsigned>(x.mod);
+  }
+  // Always 5 dims, so the kernel issues a single instruction form
+  // (cp.async.bulk.tensor.5d) whatever the operand's rank.
   const CUresult res =
-      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides, box,
-         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), gdim, gstr, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return res == CUDA_SUCCESS;
+  if (res != CUDA_SUCCESS) return fail("tensor-map encoding rejected");
+  return true;
+}
+
+// Operand layout: MN-major when the outer index's inner sub-index is
+// unit-stride (or the outer extent is 1), K-major when k's is.
+bool kmajor_of(const Group& outer, const Group& kg) {
+  return !(outer.str[0] == 1 || (outer.n == 1 && outer.ext[0] == 1)) && kg.str[0] == 1;
 }
 
 template <bool AK, bool BK_, bool TMA>
@@ -825,6 +935,20 @@ int launch_scale(const tcb_gemm_desc& d, double* C) {
   p.beta = d.beta;
   scale_kernel<<<num_sms() * 4, 256, 0, state().stream>>>(p);
   TCB_LAUNCHED();
+  return TCB_OK;
+}
+
+int check_gemm_groups(const tcb_gemm_desc& d) {
+  if (!has_groups(d)) return TCB_OK;
+  const OperandGroups g = groups_of(d);
+  CUtensorMap t;
+  MapProg prog;
+  const char* why = nullptr;
+  // any 256-byte aligned address: the maps are only encoded, never used
+  const double* base = reinterpret_cast<const double*>(uintptr_t{256});
+  if (!make_map(&t, &prog, base, kmajor_of(g.am, g.ak), g.am, g.ak, d, d.bat_sa, &why) ||
+      !make_map(&t, &prog, base, kmajor_of(g.bn, g.bk), g.bn, g.bk, d, d.bat_sb, &why))
+    return set_error(TCB_EUNSUPPORTED, std::string("gemm: index groups: ") + why);
   return TCB_OK;
 }
 
@@ -909,17 +1033,17 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     p.epoch = st.epoch;
   }
 
-  // Operand layouts: MN-major when the outer index is unit-stride.
-  const bool a_k = !(p.a_so == 1 || d.m == 1) && (p.a_sk == 1);
-  const bool b_k = !(p.b_so == 1 || d.n == 1) && (p.b_sk == 1);
+  const OperandGroups g = groups_of(d);
+  const bool a_k = kmajor_of(g.am, g.ak);
+  const bool b_k = kmajor_of(g.bn, g.bk);
   CUtensorMap ta, tb;
   std::memset(&ta, 0, sizeof ta);
   std::memset(&tb, 0, sizeof tb);
-  bool tma = make_map(&ta, A, a_k, d.m, d.k, p.a_so, p.a_sk, d, d.bat_sa, &p.a_rank, p.a_bdim) &&
-             make_map(&tb, B, b_k, d.n, d.k, p.b_so, p.b_sk, d, d.bat_sb, &p.b_rank, p.b_bdim);
-  // MN-major layout needs unit outer stride for TMA; K-major needs unit k stride.
-  if (tma && !a_k && p.a_so != 1 && d.m > 1) tma = false;
-  if (tma && !b_k && p.b_so != 1 && d.n > 1) tma = false;
+  const char* why = nullptr;
+  const bool tma = make_map(&ta, &p.pa, A, a_k, g.am, g.ak, d, d.bat_sa, &why) &&
+                   make_map(&tb, &p.pb, B, b_k, g.bn, g.bk, d, d.bat_sb, &why);
+  // index groups are read through the tensor maps only
+  if (!tma && has_groups(d)) return set_error(TCB_EUNSUPPORTED, std::string("gemm: index groups: ") + why);
 
   const int grid = static_cast<int>(std::min<int64_t>(p.units, sms));
   // TCB_TRACE=<file>: append per-CTA phase timestamps of this launch (diagnostics)

@@ -50,6 +50,8 @@ int ensure_init();  // lazily binds device 0 when tcb_init was not called
 
 // Device-side launchers (implemented in the .cu files).
 int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C);
+// Index-group descriptors: can the operand tensor maps describe them?
+int check_gemm_groups(const tcb_gemm_desc& d);
 int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const double* src,
                    double* dst);
 int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double* C);

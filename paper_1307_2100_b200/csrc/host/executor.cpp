@@ -151,9 +151,81 @@ std::unique_ptr<KernelBackend> make_backend(const std::string& name) {
 
 // --------------------------------------------------------- PreparedContraction
 
+namespace {
+
+tcb_gemm_desc desc_of(const DeviceRecipe& r) {
+  tcb_gemm_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.m = r.m;
+  d.n = r.n;
+  d.k = r.k;
+  d.a_sm = r.a_sm;
+  d.a_sk = r.a_sk;
+  d.b_sk = r.b_sk;
+  d.b_sn = r.b_sn;
+  d.c_nrow = static_cast<int32_t>(r.row_ext.size());
+  d.c_ncol = static_cast<int32_t>(r.col_ext.size());
+  for (std::size_t i = 0; i < r.row_ext.size(); ++i) {
+    d.c_row_ext[i] = r.row_ext[i];
+    d.c_row_str[i] = r.row_str[i];
+  }
+  for (std::size_t i = 0; i < r.col_ext.size(); ++i) {
+    d.c_col_ext[i] = r.col_ext[i];
+    d.c_col_str[i] = r.col_str[i];
+  }
+  d.nbatch = static_cast<int32_t>(r.bat_ext.size());
+  for (std::size_t i = 0; i < r.bat_ext.size(); ++i) {
+    d.bat_ext[i] = r.bat_ext[i];
+    d.bat_sa[i] = r.bat_sa[i];
+    d.bat_sb[i] = r.bat_sb[i];
+    d.bat_sc[i] = r.bat_sc[i];
+  }
+  d.alpha = 1.0;
+  d.beta = 0.0;
+  if (r.layout == "L4") {
+    d.g_m = static_cast<int32_t>(r.gm_ext.size());
+    d.g_n = static_cast<int32_t>(r.gn_ext.size());
+    d.g_k = static_cast<int32_t>(r.gk_ext.size());
+    for (std::size_t i = 0; i < r.gm_ext.size(); ++i) {
+      d.m_ext[i] = r.gm_ext[i];
+      d.a_m_str[i] = r.gm_sa[i];
+    }
+    for (std::size_t i = 0; i < r.gn_ext.size(); ++i) {
+      d.n_ext[i] = r.gn_ext[i];
+      d.b_n_str[i] = r.gn_sb[i];
+    }
+    for (std::size_t i = 0; i < r.gk_ext.size(); ++i) {
+      d.k_ext[i] = r.gk_ext[i];
+      d.a_k_str[i] = r.gk_sa[i];
+      d.b_k_str[i] = r.gk_sb[i];
+    }
+  }
+  return d;
+}
+
+}  // namespace
+
+namespace {
+// L4 recipes the device cannot map (the host rules mirror the device's, so
+// this is a safety net) are lowered again without index groups.
+DeviceRecipe lower_checked(const ValidatedContraction& v, bool* groups_ok) {
+  DeviceRecipe r = lower(v, *groups_ok);
+  if (r.layout == "L4") {
+    const tcb_gemm_desc d = desc_of(r);
+    if (tcb_gemm_check(&d) != TCB_OK) {
+      *groups_ok = false;
+      r = lower(v, false);
+    }
+  }
+  return r;
+}
+}  // namespace
+
+
 PreparedContraction::PreparedContraction(const ValidatedContraction& v, int device)
-    : recipe_(lower(v)), v_(v), device_(device) {
+    : v_(v), device_(device) {
   check(tcb_init(device_), "tcb_init");
+  recipe_ = lower_checked(v, &groups_ok_);
   nl_ = 1;
   for (int m = 0; m < v.left_rank(); ++m) nl_ *= v.label_at_left_mode(m).extent;
   nr_ = 1;
@@ -228,34 +300,7 @@ void PreparedContraction::run_contraction() {
   check(tcb_init(device_), "tcb_init");
   const double* a = pl_ ? pl_ : dl_;
   const double* b = pr_ ? pr_ : dr_;
-  tcb_gemm_desc d;
-  std::memset(&d, 0, sizeof d);
-  d.m = recipe_.m;
-  d.n = recipe_.n;
-  d.k = recipe_.k;
-  d.a_sm = recipe_.a_sm;
-  d.a_sk = recipe_.a_sk;
-  d.b_sk = recipe_.b_sk;
-  d.b_sn = recipe_.b_sn;
-  d.c_nrow = static_cast<int32_t>(recipe_.row_ext.size());
-  d.c_ncol = static_cast<int32_t>(recipe_.col_ext.size());
-  for (std::size_t i = 0; i < recipe_.row_ext.size(); ++i) {
-    d.c_row_ext[i] = recipe_.row_ext[i];
-    d.c_row_str[i] = recipe_.row_str[i];
-  }
-  for (std::size_t i = 0; i < recipe_.col_ext.size(); ++i) {
-    d.c_col_ext[i] = recipe_.col_ext[i];
-    d.c_col_str[i] = recipe_.col_str[i];
-  }
-  d.nbatch = static_cast<int32_t>(recipe_.bat_ext.size());
-  for (std::size_t i = 0; i < recipe_.bat_ext.size(); ++i) {
-    d.bat_ext[i] = recipe_.bat_ext[i];
-    d.bat_sa[i] = recipe_.bat_sa[i];
-    d.bat_sb[i] = recipe_.bat_sb[i];
-    d.bat_sc[i] = recipe_.bat_sc[i];
-  }
-  d.alpha = 1.0;
-  d.beta = 0.0;
+  const tcb_gemm_desc d = desc_of(recipe_);
   check(tcb_gemm(&d, a, b, do_), "contraction");
 }
 
@@ -269,41 +314,6 @@ void PreparedContraction::sync() {
   check(tcb_sync(), "sync");
 }
 
-namespace {
-
-tcb_gemm_desc desc_of(const DeviceRecipe& r) {
-  tcb_gemm_desc d;
-  std::memset(&d, 0, sizeof d);
-  d.m = r.m;
-  d.n = r.n;
-  d.k = r.k;
-  d.a_sm = r.a_sm;
-  d.a_sk = r.a_sk;
-  d.b_sk = r.b_sk;
-  d.b_sn = r.b_sn;
-  d.c_nrow = static_cast<int32_t>(r.row_ext.size());
-  d.c_ncol = static_cast<int32_t>(r.col_ext.size());
-  for (std::size_t i = 0; i < r.row_ext.size(); ++i) {
-    d.c_row_ext[i] = r.row_ext[i];
-    d.c_row_str[i] = r.row_str[i];
-  }
-  for (std::size_t i = 0; i < r.col_ext.size(); ++i) {
-    d.c_col_ext[i] = r.col_ext[i];
-    d.c_col_str[i] = r.col_str[i];
-  }
-  d.nbatch = static_cast<int32_t>(r.bat_ext.size());
-  for (std::size_t i = 0; i < r.bat_ext.size(); ++i) {
-    d.bat_ext[i] = r.bat_ext[i];
-    d.bat_sa[i] = r.bat_sa[i];
-    d.bat_sb[i] = r.bat_sb[i];
-    d.bat_sc[i] = r.bat_sc[i];
-  }
-  d.alpha = 1.0;
-  d.beta = 0.0;
-  return d;
-}
-
-}  // namespace
 
 // Streams and events of the streamed path, created once per prepared
 // contraction (creating them per call costs more than a small slab).
@@ -375,10 +385,25 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
   auto sub_recipe = [&](std::int64_t e) {
     ValidatedContraction sv = v_;
     sv.labels[static_cast<std::size_t>(label)].extent = e;
-    return lower(sv);
+    bool ok = groups_ok_;
+    return lower_checked(sv, &ok);
   };
   const std::int64_t base = E / slabs, extra = E % slabs;
   DeviceRecipe rb = sub_recipe(base), rb1 = extra ? sub_recipe(base + 1) : rb;
+  // slab recipes must permute exactly the operands the full recipe does (its
+  // permutation buffers are the ones allocated)
+  auto same_permutes = [&](const DeviceRecipe& x) {
+    if (x.permutes.size() != recipe_.permutes.size()) return false;
+    for (std::size_t i = 0; i < x.permutes.size(); ++i)
+      if (x.permutes[i].right != recipe_.permutes[i].right) return false;
+    return true;
+  };
+  if (!same_permutes(rb) || !same_permutes(rb1)) {
+    upload(left, right);
+    run();
+    download(out);
+    return 1;
+  }
 
   if (!pipes_) {
     pipes_ = std::make_unique<Pipes>();

@@ -15,14 +15,21 @@
 //     are permuted on the device into [M|N, K] or [K, M|N] order, keeping each
 //     operand's unit-stride label innermost so the permutation copies
 //     contiguous runs (cfg3: A[a,k,c,l] -> A'[a,c,l,k], B[l,b,k,d] -> B'[l,k,b,d]).
+//   * L4 — instead of L3 where the GEMM's tensor maps can describe the groups
+//     directly: M = all left free labels, N = all right free labels, K = all
+//     contracted labels, each a composite of operand dimensions whose inner
+//     sub-index tiles the kernel's TMA boxes (cfg3 reads A[a,k,c,l] and
+//     B[l,b,k,d] in place: M=(a,c), N=(b,d), K=(l,k)). No permutation pass.
 // The output is never permuted: the GEMM epilogue addresses C through the
 // composite row (M labels) and column (N labels) strides. Extent-1 labels are
 // dropped first (any coordinate of them is 0).
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <sstream>
 
 #include "tc/contract.hpp"
+#include "tcb.h"
 
 namespace tc {
 namespace {
@@ -92,18 +99,147 @@ void push_group(const ValidatedContraction& v, const std::vector<int>& ids,
   }
 }
 
+// Sub-indices of a group: consecutive labels merged where they chain in
+// every operand they address (stride[next] == stride[prev] * extent[prev]).
+struct SubIdx {
+  std::vector<std::int64_t> ext, sa, sb;
+};
+SubIdx sub_indices(const ValidatedContraction& v, const std::vector<int>& ids,
+                   const std::vector<std::int64_t>& sa, const std::vector<std::int64_t>& sb,
+                   bool use_a, bool use_b) {
+  SubIdx g;
+  for (int id : ids) {
+    const std::int64_t e = v.labels[static_cast<std::size_t>(id)].extent;
+    const std::int64_t a = sa[static_cast<std::size_t>(id)], b = sb[static_cast<std::size_t>(id)];
+    if (!g.ext.empty() && (!use_a || g.sa.back() * g.ext.back() == a) &&
+        (!use_b || g.sb.back() * g.ext.back() == b)) {
+      g.ext.back() *= e;
+      continue;
+    }
+    g.ext.push_back(e);
+    g.sa.push_back(use_a ? a : 0);
+    g.sb.push_back(use_b ? b : 0);
+  }
+  return g;
+}
+
+// Can one operand's tensor map carry (outer group, k group)? Mirrors the
+// box rules of make_map (device/gemm_dmma.cu): the unit-stride sub-index
+// leads with a 16-element box; the other group's inner sub-index is boxed 16
+// (MN-major) or 128 (K-major, possibly spilling into its next sub-index);
+// inner extents of multi-index groups must tile those boxes; at most 5 dims,
+// even strides (16-byte multiples), extents below 2^31.
+bool fits_map(const std::vector<std::int64_t>& oe, const std::vector<std::int64_t>& os,
+              const std::vector<std::int64_t>& ke, const std::vector<std::int64_t>& ks) {
+  if (oe.empty() || ke.empty() || oe.size() + ke.size() > 5) return false;
+  const bool kmajor = os[0] != 1;
+  if (kmajor && ks[0] != 1) return false;
+  const auto& le = kmajor ? ke : oe;
+  const auto& xe = kmajor ? oe : ke;
+  if (le.size() > 1 && le[0] % 16) return false;
+  const std::int64_t box = kmajor ? 128 : 16;
+  if (xe.size() > 1 && xe[0] % box) {
+    if (!kmajor || box % xe[0]) return false;
+    if (xe.size() > 2 && xe[1] % (box / xe[0])) return false;
+  }
+  auto strides_ok = [](const std::vector<std::int64_t>& e, const std::vector<std::int64_t>& s,
+                       bool lead) {
+    for (std::size_t i = 0; i < e.size(); ++i) {
+      if (e[i] >= (1LL << 31)) return false;
+      if (lead && i == 0) continue;
+      if (e[i] > 1 && (s[i] <= 0 || s[i] % 2 || s[i] * 8 >= (1LL << 40))) return false;
+    }
+    return true;
+  };
+  return strides_ok(oe, os, !kmajor) && strides_ok(ke, ks, kmajor);
+}
+
+// The L4 recipe, or false when the groups do not fit the tensor maps.
+bool lower_groups(const ValidatedContraction& v, const Side& A, const Side& B,
+                  const std::vector<std::int64_t>& ostr, DeviceRecipe& r) {
+  auto is_k = [&](int id) { return v.labels[static_cast<std::size_t>(id)].contracted; };
+  if (A.modes.empty() || B.modes.empty()) return false;
+  const int ua = A.modes[0], ub = B.modes[0];
+  std::vector<int> kl, ml, nl;
+  for (int id : A.modes) (is_k(id) ? kl : ml).push_back(id);
+  for (int id : B.modes)
+    if (!is_k(id)) nl.push_back(id);
+  if (kl.empty() || ml.empty() || nl.empty()) return false;
+  // k's inner sub-index: the unit-stride label of a K-major operand (both
+  // K-major on different labels = class 3.1: no common order, permute)
+  int kin = -1;
+  if (is_k(ua) && is_k(ub) && ua != ub) return false;
+  if (is_k(ua)) kin = ua;
+  else if (is_k(ub)) kin = ub;
+  else {
+    kin = kl[0];
+    for (int id : kl)
+      if (v.labels[static_cast<std::size_t>(id)].extent % 16 == 0) {
+        kin = id;
+        break;
+      }
+  }
+  std::vector<int> korder{kin};
+  for (int id : kl)
+    if (id != kin) korder.push_back(id);
+  const SubIdx K = sub_indices(v, korder, A.stride, B.stride, true, true);
+  const SubIdx M = sub_indices(v, ml, A.stride, B.stride, true, false);
+  const SubIdx N = sub_indices(v, nl, A.stride, B.stride, false, true);
+  if (K.ext.size() > TCB_MAX_DIMS || M.ext.size() > TCB_MAX_DIMS || N.ext.size() > TCB_MAX_DIMS)
+    return false;
+  if (!fits_map(M.ext, M.sa, K.ext, K.sa) || !fits_map(N.ext, N.sb, K.ext, K.sb)) return false;
+  r.m = product(v, ml);
+  r.n = product(v, nl);
+  r.k = product(v, korder);
+  if (r.m < 2 || r.n < 2) return false;  // GEMV shapes take the plain strides
+  r.a_sm = M.sa[0];
+  r.a_sk = K.sa[0];
+  r.b_sk = K.sb[0];
+  r.b_sn = N.sb[0];
+  r.gm_ext = M.ext;
+  r.gm_sa = M.sa;
+  r.gn_ext = N.ext;
+  r.gn_sb = N.sb;
+  r.gk_ext = K.ext;
+  r.gk_sa = K.sa;
+  r.gk_sb = K.sb;
+  push_group(v, ml, ostr, r.row_ext, r.row_str);
+  push_group(v, nl, ostr, r.col_ext, r.col_str);
+  r.layout = "L4";
+  return true;
+}
+
 }  // namespace
 
 std::string DeviceRecipe::summary() const {
   std::ostringstream os;
-  os << layout << " gemm m=" << m << " n=" << n << " k=" << k << " a(" << a_sm << "," << a_sk
-     << ") b(" << b_sk << "," << b_sn << ") batch=[";
+  os << layout << " gemm m=" << m << " n=" << n << " k=" << k;
+  if (layout == "L4") {
+    auto grp = [&](const char* name, const std::vector<std::int64_t>& e,
+                   const std::vector<std::int64_t>& s1, const std::vector<std::int64_t>* s2) {
+      os << ' ' << name << '[';
+      for (std::size_t i = 0; i < e.size(); ++i) {
+        os << (i ? "," : "") << e[i] << ':' << s1[i];
+        if (s2) os << '/' << (*s2)[i];
+      }
+      os << ']';
+    };
+    grp("m", gm_ext, gm_sa, nullptr);
+    grp("n", gn_ext, gn_sb, nullptr);
+    grp("k", gk_ext, gk_sa, &gk_sb);
+    os << " batch=[] permutes=0";
+    return os.str();
+  }
+  os << " a(" << a_sm << "," << a_sk << ") b(" << b_sk << "," << b_sn << ") batch=[";
   for (std::size_t i = 0; i < bat_ext.size(); ++i) os << (i ? "," : "") << bat_ext[i];
   os << "] permutes=" << permutes.size();
   return os.str();
 }
 
-DeviceRecipe lower(const ValidatedContraction& v) {
+DeviceRecipe lower(const ValidatedContraction& v, bool index_groups) {
+  // TC_INDEX_GROUPS=0 disables L4 (A/B comparisons against L3)
+  if (const char* env = std::getenv("TC_INDEX_GROUPS"); env != nullptr && env[0] == '0')
+    index_groups = false;
   const std::size_t nlab = v.labels.size();
   Side A = side_of(v, false), B = side_of(v, true);
   std::vector<std::int64_t> ostr(nlab, 0);
@@ -155,6 +291,8 @@ DeviceRecipe lower(const ValidatedContraction& v) {
   }
 
   DeviceRecipe r;
+  if ((perm_a || perm_b) && index_groups && lower_groups(v, A, B, ostr, r)) return r;
+  r = DeviceRecipe{};
   r.k = product(v, korder);
   std::vector<int> mgroup, ngroup, batch;
 

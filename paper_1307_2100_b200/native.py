@@ -32,7 +32,12 @@ class GemmDesc(C.Structure):
                 ("nbatch", C.c_int32),
                 ("bat_ext", i64 * TCB_MAX_DIMS), ("bat_sa", i64 * TCB_MAX_DIMS),
                 ("bat_sb", i64 * TCB_MAX_DIMS), ("bat_sc", i64 * TCB_MAX_DIMS),
-                ("alpha", f64), ("beta", f64)]
+                ("alpha", f64), ("beta", f64),
+                ("g_m", C.c_int32), ("g_n", C.c_int32), ("g_k", C.c_int32),
+                ("m_ext", i64 * TCB_MAX_DIMS), ("a_m_str", i64 * TCB_MAX_DIMS),
+                ("n_ext", i64 * TCB_MAX_DIMS), ("b_n_str", i64 * TCB_MAX_DIMS),
+                ("k_ext", i64 * TCB_MAX_DIMS), ("a_k_str", i64 * TCB_MAX_DIMS),
+                ("b_k_str", i64 * TCB_MAX_DIMS)]
 
 
 class GemmInfo(C.Structure):
@@ -67,6 +72,7 @@ TCB_API = {
     "tcb_memcpy_async": (i32, [vp, vp, i64, vp]),
     "tcb_host_is_pinned": (i32, [vp, C.POINTER(C.c_int)]),
     "tcb_gemm": (i32, [C.POINTER(GemmDesc), vp, vp, vp]),
+    "tcb_gemm_check": (i32, [C.POINTER(GemmDesc)]),
     "tcb_last_gemm_info": (i32, [C.POINTER(GemmInfo)]),
     "tcb_dgemm": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64]),
     "tcb_dgemm_strided_batched": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, i64, vp, i64,

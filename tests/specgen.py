@@ -9,7 +9,10 @@ import numpy as np
 POOL = list("abcdefgh")
 
 
-def random_spec(rng: np.random.Generator, max_extent: int = 6, max_rank: int = 4):
+def random_spec(rng: np.random.Generator, max_extent: int = 6, max_rank: int = 4,
+                extents=None):
+    """A random valid contraction; label extents uniform in [1, max_extent],
+    or drawn from the `extents` sequence when given."""
     while True:
         lrank = int(rng.integers(2, max_rank + 1))
         rrank = int(rng.integers(2, max_rank + 1))
@@ -40,7 +43,8 @@ def random_spec(rng: np.random.Generator, max_extent: int = 6, max_rank: int = 4
         expr = f"R[{','.join(outs)}] = A[{','.join(lidx)}] * B[{','.join(ridx)}]"
         ext = {}
         for tok in lidx + ridx:
-            ext.setdefault(tok[1:], int(rng.integers(1, max_extent + 1)))
+            ext.setdefault(tok[1:], int(rng.choice(extents)) if extents is not None
+                           else int(rng.integers(1, max_extent + 1)))
         extents = ",".join(f"{k}={v}" for k, v in ext.items())
         return expr, extents
 
