@@ -69,14 +69,19 @@ static_assert(STAGES_STAGED * STAGE_BYTES + STAGING_BYTES + TAIL_BYTES + 512 <= 
               "staged layout must fit with alignment slack");
 
 // How the producer derives the 5 coordinates of an operand tensor map from
-// the (outer index, k index, batch index) of a box origin: dimension d reads
+// the (outer index, k index, batch index) of a tile origin: dimension d reads
 // source src[d] (0 outer, 1 k, 2 batch, 3 constant 0) and takes
 // (value / div[d]) % mod[d] (mod 0: no modulus). Composite index groups —
 // several tensor dimensions forming one GEMM index — are thereby read in
-// place, with no permutation pass.
+// place, with no permutation pass. Outer and batch coordinates are computed
+// once per work unit, k coordinates once per stage. nbox: 1 when one box
+// covers the operand's whole stage; 8 for MN-major operands whose outer
+// extent is not a multiple of 16 (eight 16x16 boxes, dimension 0 advancing
+// by 16).
 struct MapProg {
   unsigned div[5], mod[5];
   int src[5];
+  int nbox;
 };
 
 struct Params {
@@ -235,6 +240,23 @@ __device__ __forceinline__ int64_t composite(int64_t idx64, int n, const int64_t
   return off + static_cast<int64_t>(idx) * str[n - 1];
 }
 
+// Outer and batch coordinates of a tile origin (k dims: 0).
+__device__ __forceinline__ void unit_coords(const MapProg& g, unsigned o, unsigned b,
+                                            int (&c)[5]) {
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    const int s = g.src[d];
+    if (g.src[d] == 0 || g.src[d] == 2) {
+      unsigned v = s == 0 ? o : b;
+      if (g.div[d] != 1u) v /= g.div[d];
+      if (g.mod[d] != 0u) v %= g.mod[d];
+      c[d] = static_cast<int>(v);
+    } else {
+      c[d] = 0;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 // Producer-side iterator over this CTA's (unit, k-block) sequence. All
 // per-unit address math (64-bit divisions) happens once per unit here, in the
@@ -244,7 +266,7 @@ struct LoadIter {
   int kb, kb1;
   int m0, n0;            // tile origin (TMA coordinates are int32)
   int64_t oa, ob;        // batch offsets (cp.async path)
-  unsigned batch;        // batch index (TMA path: decoded by the map programs)
+  int ca[5], cb[5];      // TMA: outer + batch coordinates of the unit's tiles
   bool valid;
 
   template <bool USE_TMA>
@@ -252,16 +274,18 @@ struct LoadIter {
     valid = u < p.units;
     if (!valid) return;
     const Unit un = decode_unit(p, u);
-    batch = un.batch;
-    if (!USE_TMA) {
-      int bc[TCB_MAX_DIMS];
-      int64_t oc;
-      batch_offsets(p, un.batch, oa, ob, oc, bc);
-    }
     kb = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
     kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
     m0 = un.tm * BM;
     n0 = un.tn * BN;
+    if (USE_TMA) {
+      unit_coords(p.pa, static_cast<unsigned>(m0), un.batch, ca);
+      unit_coords(p.pb, static_cast<unsigned>(n0), un.batch, cb);
+    } else {
+      int bc[TCB_MAX_DIMS];
+      int64_t oc;
+      batch_offsets(p, un.batch, oa, ob, oc, bc);
+    }
   }
   template <bool USE_TMA>
   __device__ __forceinline__ void advance(const Params& p) {
@@ -272,16 +296,14 @@ struct LoadIter {
   }
 };
 
-__device__ __forceinline__ void map_coords(const MapProg& g, unsigned o, unsigned k, unsigned b,
-                                           int (&c)[5]) {
-#pragma unroll
-  for (int d = 0; d < 5; ++d) {
-    const int s = g.src[d];
-    unsigned v = s == 0 ? o : (s == 1 ? k : (s == 2 ? b : 0u));
-    if (g.div[d] != 1u) v /= g.div[d];
-    if (g.mod[d] != 0u) v %= g.mod[d];
-    c[d] = static_cast<int>(v);
-  }
+__device__ __forceinline__ unsigned prog_coord(const MapProg& g, int d, unsigned v) {
+  if (g.div[d] != 1u) v /= g.div[d];
+  if (g.mod[d] != 0u) v %= g.mod[d];
+  return v;
+}
+// k coordinate of dimension d at k index k0 (0 for outer / batch dims)
+__device__ __forceinline__ int k_coord(const MapProg& g, int d, unsigned k0) {
+  return g.src[d] == 1 ? static_cast<int>(prog_coord(g, d, k0)) : 0;
 }
 
 // Issue one k-block of both operands into a stage. TMA: one thread, 5-D maps
@@ -294,17 +316,22 @@ __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& 
   const uint32_t sB = sA + STAGE_A;
   if (USE_TMA) {
     mbar_expect_tx(full, STAGE_BYTES);
-    int c[5];
-    // K-major: one 16(k) x 128(outer) box; MN-major: 8 boxes of 16 x 16
+    const unsigned k0u = static_cast<unsigned>(k0);
+    {
+      int c[5];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) c[d] = li.ca[d] + k_coord(p.pa, d, k0u);
 #pragma unroll 1
-    for (int i = 0; i < (A_KMAJOR ? 1 : BM / 16); ++i) {
-      map_coords(p.pa, li.m0 + 16 * i, k0, li.batch, c);
-      tma_load5(sA + i * 2048, &tmA, full, c[0], c[1], c[2], c[3], c[4]);
+      for (int i = 0; i < p.pa.nbox; ++i, c[0] += 16)
+        tma_load5(sA + i * 2048, &tmA, full, c[0], c[1], c[2], c[3], c[4]);
     }
+    {
+      int c[5];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) c[d] = li.cb[d] + k_coord(p.pb, d, k0u);
 #pragma unroll 1
-    for (int i = 0; i < (B_KMAJOR ? 1 : BN / 16); ++i) {
-      map_coords(p.pb, li.n0 + 16 * i, k0, li.batch, c);
-      tma_load5(sB + i * 2048, &tmB, full, c[0], c[1], c[2], c[3], c[4]);
+      for (int i = 0; i < p.pb.nbox; ++i, c[0] += 16)
+        tma_load5(sB + i * 2048, &tmB, full, c[0], c[1], c[2], c[3], c[4]);
     }
   } else {
     const double* Ab = p.A + li.oa;
@@ -783,14 +810,19 @@ OperandGroups groups_of(const tcb_gemm_desc& d) {
 }
 bool has_groups(const tcb_gemm_desc& d) { return d.g_m > 0 || d.g_n > 0 || d.g_k > 0; }
 
-// Build the tensor map of one operand and its coordinate program. Dimension
-// order: [lead inner: the unit-stride sub-index, box 16] [other inner: box 16
-// (MN-major) or 128 (K-major), spilling into the next sub-index when the inner
-// extent divides 128] [remaining sub-indices, box 1] [batch dims with a
-// non-zero stride, box 1]. Box rows never straddle a sub-index boundary: inner
-// extents of multi-dimension groups must be multiples of the box (or, K-major,
-// divide 128). Returns false with `why` set when TMA cannot describe the
-// operand; plain descriptors then fall back to cp.async.
+// Build the tensor map of one operand and its coordinate program.
+//   K-major:  [k inner: box 16] [outer: box spanning 128 indices] ...
+//   MN-major: [outer % 16: box 16] [k inner: box 16] [outer / 16: box spanning
+//             the 8 16-row chunks of the tile] ...
+// then the remaining sub-indices (box 1) and the batch dims with a non-zero
+// stride (box 1). A span may cover a whole sub-index whose extent divides it
+// and continue into the next one; span boundaries never cut a box row, so
+// inner extents of multi-index groups must be multiples of 16 (and of 128 /
+// divisors of 128 where they are spanned). One TMA instruction then loads an
+// operand's whole stage. MN-major operands with an outer extent that is not a
+// multiple of 16 (plain descriptors only) use eight 16x16 boxes instead.
+// Returns false with `why` set when TMA cannot describe the operand; plain
+// descriptors then fall back to cp.async.
 bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
               const Group& outer, const Group& kg, const tcb_gemm_desc& d, const int64_t* bstr,
               const char** why) {
@@ -813,40 +845,88 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
     if (r < 16) dims[r] = Dim{ext, str, box, src, div, mod};
     ++r;
   };
+  // Sub-indices [from, n) of group g (index value = source / div0), the
+  // first `span` values of each tile covered by boxes; returns the next div.
+  auto push_span = [&](const Group& g, int from, int64_t span, int src, int64_t div0,
+                       const char** err) -> bool {
+    const int n = g.n - from;
+    const int64_t e0 = g.ext[from];
+    int used = 1;
+    int64_t div = div0;
+    if (n == 1 || e0 % span == 0) {
+      push(e0, g.str[from], static_cast<uint32_t>(span), src, div, n > 1 ? e0 : 0);
+      div *= e0;
+    } else if (span % e0 == 0) {
+      const int64_t e1 = g.ext[from + 1], b1 = span / e0;
+      if (n > 2 && e1 % b1) {
+        *err = "second extent of a group does not tile the box";
+        return false;
+      }
+      push(e0, g.str[from], static_cast<uint32_t>(e0), src, div, e0);
+      push(e1, g.str[from + 1], static_cast<uint32_t>(b1), src, div * e0, n > 2 ? e1 : 0);
+      div *= e0 * e1;
+      used = 2;
+    } else {
+      *err = "inner extent of a group does not tile the box";
+      return false;
+    }
+    for (int j = from + used; j < g.n; ++j) {
+      push(g.ext[j], g.str[j], 1, src, div, j + 1 < g.n ? g.ext[j] : 0);
+      div *= g.ext[j];
+    }
+    return true;
+  };
+  auto push_rest = [&](const Group& g, int src) {
+    int64_t div = g.ext[0];
+    for (int j = 1; j < g.n; ++j) {
+      push(g.ext[j], g.str[j], 1, src, div, j + 1 < g.n ? g.ext[j] : 0);
+      div *= g.ext[j];
+    }
+  };
+  auto push_batch = [&]() {
+    int64_t div = 1;
+    for (int i = 0; i < d.nbatch; ++i) {
+      if (bstr[i] != 0 && d.bat_ext[i] > 1) push(d.bat_ext[i], bstr[i], 1, 2, div, d.bat_ext[i]);
+      div *= d.bat_ext[i];
+    }
+  };
   const Group& lead = kmajor ? kg : outer;
-  const Group& other = kmajor ? outer : kg;
-  const int lsrc = kmajor ? 1 : 0, osrc = kmajor ? 0 : 1;
   if (lead.str[0] != 1 && lead.ext[0] > 1) return fail("no unit-stride inner index");
-  if (lead.n > 1 && lead.ext[0] % 16) return fail("inner extent of a unit-stride group not a multiple of 16");
-  push(lead.ext[0], 1, 16, lsrc, 1, lead.n > 1 ? lead.ext[0] : 0);
-  const uint32_t obox = kmajor ? BN : 16;
-  const int64_t e0 = other.ext[0];
-  int rest = 1;
-  int64_t div = e0;
-  if (other.n > 1 && e0 % obox) {
-    if (!kmajor || obox % e0) return fail("inner extent of a strided group does not tile the box");
-    const int64_t e1 = other.ext[1], b1 = obox / e0;
-    if (other.n > 2 && e1 % b1) return fail("second extent of a strided group does not tile the box");
-    push(e0, other.str[0], static_cast<uint32_t>(e0), osrc, 1, e0);
-    push(e1, other.str[1], static_cast<uint32_t>(b1), osrc, e0, other.n > 2 ? e1 : 0);
-    rest = 2;
-    div = e0 * e1;
+  if (kg.n > 1 && kg.ext[0] % 16) return fail("inner extent of a k group not a multiple of 16");
+  const char* err = nullptr;
+  prog->nbox = 1;
+  if (kmajor) {
+    push(kg.ext[0], 1, 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
+    if (!push_span(outer, 0, BN, 0, 1, &err)) return fail(err);
+    push_rest(kg, 1);
+    push_batch();
   } else {
-    push(e0, other.str[0], obox, osrc, 1, other.n > 1 ? e0 : 0);
-  }
-  for (int j = rest; j < other.n; ++j) {
-    push(other.ext[j], other.str[j], 1, osrc, div, j + 1 < other.n ? other.ext[j] : 0);
-    div *= other.ext[j];
-  }
-  div = lead.ext[0];
-  for (int j = 1; j < lead.n; ++j) {
-    push(lead.ext[j], lead.str[j], 1, lsrc, div, j + 1 < lead.n ? lead.ext[j] : 0);
-    div *= lead.ext[j];
-  }
-  div = 1;
-  for (int i = 0; i < d.nbatch; ++i) {
-    if (bstr[i] != 0 && d.bat_ext[i] > 1) push(d.bat_ext[i], bstr[i], 1, 2, div, d.bat_ext[i]);
-    div *= d.bat_ext[i];
+    const int64_t e0 = outer.ext[0];
+    bool spanned = false;
+    if (e0 % 16 == 0) {
+      // the outer group as (outer % 16, outer / 16 = (e0/16, e1, ...))
+      Group hi = outer;
+      hi.ext[0] = e0 / 16;
+      hi.str[0] = 16 * outer.str[0];
+      int from = (hi.ext[0] == 1 && hi.n > 1) ? 1 : 0;
+      push(16, 1, 16, 0, 1, 16);
+      push(kg.ext[0], kg.str[0], 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
+      if (!push_span(hi, from, BM / 16, 0, 16, &err)) return fail(err);
+      push_rest(kg, 1);
+      push_batch();
+      spanned = r <= 5;
+      if (!spanned && outer.n > 1) return fail("more than 5 tensor-map dimensions");
+    } else if (outer.n > 1) {
+      return fail("inner extent of a unit-stride group not a multiple of 16");
+    }
+    if (!spanned) {  // plain operand: eight 16 x 16 boxes per stage
+      r = 0;
+      prog->nbox = BM / 16;
+      push(e0, 1, 16, 0, 1, 0);
+      push(kg.ext[0], kg.str[0], 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
+      push_rest(kg, 1);
+      push_batch();
+    }
   }
   if (r > 5) return fail("more than 5 tensor-map dimensions");
   cuuint64_t gdim[5], gstr[4];
@@ -859,7 +939,8 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
     box[i] = x.box;
     if (i > 0) {
       const int64_t st = x.ext > 1 ? x.str : 2;  // extent-1 dims: any legal stride
-      if (st <= 0 || st % 2 || st * 8 >= (1LL << 40)) return fail("stride not a positive multiple of 16 bytes");
+      if (st <= 0 || st % 2 || st * 8 >= (1LL << 40))
+        return fail("stride not a positive multiple of 16 bytes");
       gstr[i - 1] = static_cast<cuuint64_t>(st * 8);
     }
     prog->src[i] = x.src;

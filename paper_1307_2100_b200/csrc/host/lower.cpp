@@ -125,23 +125,40 @@ SubIdx sub_indices(const ValidatedContraction& v, const std::vector<int>& ids,
 
 // Can one operand's tensor map carry (outer group, k group)? Mirrors the
 // box rules of make_map (device/gemm_dmma.cu): the unit-stride sub-index
-// leads with a 16-element box; the other group's inner sub-index is boxed 16
-// (MN-major) or 128 (K-major, possibly spilling into its next sub-index);
-// inner extents of multi-index groups must tile those boxes; at most 5 dims,
-// even strides (16-byte multiples), extents below 2^31.
+// leads; k's inner sub-index is boxed 16; the outer index is spanned 128 at a
+// time (K-major) or split as (outer % 16, outer / 16) with the 8 chunks of a
+// tile spanned (MN-major). A span covers a sub-index whose extent it divides
+// (or is a multiple of) and may continue into the next; at most 5 dims, even
+// strides (16-byte multiples), extents below 2^31.
 bool fits_map(const std::vector<std::int64_t>& oe, const std::vector<std::int64_t>& os,
               const std::vector<std::int64_t>& ke, const std::vector<std::int64_t>& ks) {
-  if (oe.empty() || ke.empty() || oe.size() + ke.size() > 5) return false;
+  if (oe.empty() || ke.empty()) return false;
   const bool kmajor = os[0] != 1;
   if (kmajor && ks[0] != 1) return false;
-  const auto& le = kmajor ? ke : oe;
-  const auto& xe = kmajor ? oe : ke;
-  if (le.size() > 1 && le[0] % 16) return false;
-  const std::int64_t box = kmajor ? 128 : 16;
-  if (xe.size() > 1 && xe[0] % box) {
-    if (!kmajor || box % xe[0]) return false;
-    if (xe.size() > 2 && xe[1] % (box / xe[0])) return false;
+  if (ke.size() > 1 && ke[0] % 16) return false;
+  // span rule over group g (first sub-index g0) covering `span` values
+  auto spans = [](std::vector<std::int64_t> g, std::int64_t span) {
+    if (g.size() == 1 || g[0] % span == 0) return true;
+    if (span % g[0]) return false;
+    return g.size() <= 2 || g[1] % (span / g[0]) == 0;
+  };
+  std::size_t dims = 0;
+  if (kmajor) {
+    if (!spans(oe, 128)) return false;
+    dims = 1 + oe.size() + (ke.size() - 1);
+  } else {
+    if (oe.size() > 1 && oe[0] % 16) return false;
+    if (oe[0] % 16 == 0) {
+      std::vector<std::int64_t> hi(oe);
+      hi[0] /= 16;
+      if (hi[0] == 1 && hi.size() > 1) hi.erase(hi.begin());
+      if (!spans(hi, 8)) return false;
+      dims = 2 + hi.size() + (ke.size() - 1);
+    } else {
+      dims = 2 + (ke.size() - 1);  // plain: eight 16 x 16 boxes
+    }
   }
+  if (dims > 5) return false;
   auto strides_ok = [](const std::vector<std::int64_t>& e, const std::vector<std::int64_t>& s,
                        bool lead) {
     for (std::size_t i = 0; i < e.size(); ++i) {

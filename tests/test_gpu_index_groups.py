@@ -38,7 +38,7 @@ CASES = [
     # both K-major on the same label, M and N composite (class 3.2)
     ("C[+a,+b,+c,+d] = A[+k,+a,+l,+c] * B[-k,+b,-l,+d]", "a=32,b=64,c=3,d=2,k=16,l=3"),
     # tails: outer groups not a multiple of the 128 tile, K not a multiple of 16 outside the inner
-    ("C[+a,+c,+b] = A[+a,+k,+c,+l] * B[-l,+b,-k]", "a=48,b=40,c=3,k=5,l=16"),
+    ("C[+a,+c,+b] = A[+a,+k,+c,+l] * B[-l,+b,-k]", "a=32,b=40,c=5,k=5,l=16"),
 ]
 
 
@@ -73,7 +73,7 @@ def test_random_l4_family(dev):
 
 
 def test_l4_prepared_and_streamed_paths(dev):
-    e, x = "C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]", "a=64,b=64,c=24,d=40,k=8,l=32"
+    e, x = "C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]", "a=64,b=64,c=12,d=20,k=4,l=32"
     L, R = O.operands(e, x, 1)
     want = O.naive(e, x, L, R)
     p = T.Prepared(e, x)
