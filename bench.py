@@ -35,6 +35,7 @@ import statistics
 import subprocess
 import sys
 import time
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -118,6 +119,8 @@ def pinned_array(n: int, dev) -> np.ndarray:
         check = dev.tcb_host_register(a.ctypes.data, a.nbytes)
         if check != 0:
             raise RuntimeError(dev.tcb_last_error().decode())
+        # unregister before numpy frees the memory (never leave it registered)
+        weakref.finalize(a, dev.tcb_host_unregister, a.ctypes.data)
     return a
 
 

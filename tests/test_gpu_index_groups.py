@@ -84,11 +84,14 @@ def test_l4_prepared_and_streamed_paths(dev):
     p.download(out)
     assert close(out, want)
     # streamed over the output's outermost label (d: outermost in B)
-    for arr in (L, R):
-        T.check(dev.tcb_host_register(arr.ctypes.data, arr.nbytes))
     outs = np.zeros(want.size)
-    T.check(dev.tcb_host_register(outs.ctypes.data, outs.nbytes))
-    used = p.run_streamed(L, R, outs, slabs=5)
+    for arr in (L, R, outs):
+        T.check(dev.tcb_host_register(arr.ctypes.data, arr.nbytes))
+    try:
+        used = p.run_streamed(L, R, outs, slabs=5)
+    finally:
+        for arr in (L, R, outs):  # never leave freed memory registered
+            dev.tcb_host_unregister(arr.ctypes.data)
     assert used == 5
     assert close(outs, want)
 

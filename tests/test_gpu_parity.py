@@ -190,11 +190,14 @@ def test_streamed_host_path_matches(dev, name, e, x):
     p = T.Prepared(e, x)
     inf = p.info()
     L, R = O.operands(e, x, 1)
-    for a in (L, R):
-        T.check(dev.tcb_host_register(a.ctypes.data, a.nbytes))
     out = np.zeros(inf["output"])
-    T.check(dev.tcb_host_register(out.ctypes.data, out.nbytes))
-    used = p.run_streamed(L, R, out, slabs=5)
+    for a in (L, R, out):
+        T.check(dev.tcb_host_register(a.ctypes.data, a.nbytes))
+    try:
+        used = p.run_streamed(L, R, out, slabs=5)
+    finally:
+        for a in (L, R, out):  # never leave freed memory registered
+            dev.tcb_host_unregister(a.ctypes.data)
     assert used == 5, name
     assert O.max_rel_error(out, O.naive(e, x, L, R)) <= TOL
     ref = np.empty_like(out)
