@@ -82,6 +82,7 @@ struct MapProg {
   unsigned div[5], mod[5];
   int src[5];
   int nbox;
+  int kdim;   // the single k dim when k is not composite (coordinate = k), else -1
 };
 
 struct Params {
@@ -319,16 +320,26 @@ __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& 
     const unsigned k0u = static_cast<unsigned>(k0);
     {
       int c[5];
+      if (p.pa.kdim >= 0) {
 #pragma unroll
-      for (int d = 0; d < 5; ++d) c[d] = li.ca[d] + k_coord(p.pa, d, k0u);
+        for (int d = 0; d < 5; ++d) c[d] = li.ca[d] + (d == p.pa.kdim ? k0 : 0);
+      } else {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) c[d] = li.ca[d] + k_coord(p.pa, d, k0u);
+      }
 #pragma unroll 1
       for (int i = 0; i < p.pa.nbox; ++i, c[0] += 16)
         tma_load5(sA + i * 2048, &tmA, full, c[0], c[1], c[2], c[3], c[4]);
     }
     {
       int c[5];
+      if (p.pb.kdim >= 0) {
 #pragma unroll
-      for (int d = 0; d < 5; ++d) c[d] = li.cb[d] + k_coord(p.pb, d, k0u);
+        for (int d = 0; d < 5; ++d) c[d] = li.cb[d] + (d == p.pb.kdim ? k0 : 0);
+      } else {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) c[d] = li.cb[d] + k_coord(p.pb, d, k0u);
+      }
 #pragma unroll 1
       for (int i = 0; i < p.pb.nbox; ++i, c[0] += 16)
         tma_load5(sB + i * 2048, &tmB, full, c[0], c[1], c[2], c[3], c[4]);
@@ -903,7 +914,9 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
   } else {
     const int64_t e0 = outer.ext[0];
     bool spanned = false;
-    if (e0 % 16 == 0) {
+    // TCB_BOXES8=1 (diagnostics): plain MN-major operands as eight 16x16 boxes
+    static const bool boxes8 = getenv("TCB_BOXES8") != nullptr;
+    if (e0 % 16 == 0 && !(boxes8 && outer.n == 1)) {
       // the outer group as (outer % 16, outer / 16 = (e0/16, e1, ...))
       Group hi = outer;
       hi.ext[0] = e0 / 16;
@@ -947,6 +960,10 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
     prog->div[i] = static_cast<unsigned>(x.div);
     prog->mod[i] = static_cast<unsigned>(x.mod);
   }
+  prog->kdim = -1;
+  if (kg.n == 1)
+    for (int i = 0; i < 5; ++i)
+      if (prog->src[i] == 1) prog->kdim = i;
   // Always 5 dims, so the kernel issues a single instruction form
   // (cp.async.bulk.tensor.5d) whatever the operand's rank.
   const CUresult res =
