@@ -104,8 +104,13 @@ struct Params {
   unsigned* counters;
   unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
   unsigned long long* trace;  // TCB_TRACE diagnostics: per-CTA phase timestamps (or null)
+  int diag;                   // TCB_DIAG bits (diagnostics only): 1 = storers skip C writes
   // TMA coordinate programs of the A and B tensor maps (see MapProg)
   MapProg pa, pb;
+  // staged epilogue: C written by one TMA tensor store per tile (c_tma) with
+  // coordinate program pc (sources: 0 m origin, 1 n origin, 2 batch)
+  int c_tma;
+  MapProg pc;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -147,12 +152,40 @@ __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_store5(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                           int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
+      " [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// all bulk stores are complete (visible in global memory)
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// order this thread's generic-proxy shared-memory writes before async-proxy reads
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Byte offset of accumulator (m, n) of a tile in the staging buffer: 8 boxes
+// (m / 16) of [n 128][m 16] with the 128-byte swizzle — the smem image of
+// the output tensor map's box, conflict-free for the consumers' fragment
+// stores and for the fallback storers' column reads.
+__device__ __forceinline__ uint32_t stage_off(int m, int n) {
+  return (m >> 4) * 16384 + n * 128 + (((((m & 15) >> 1) ^ (n & 7))) << 4) + ((m & 1) << 3);
+}
 // Diagnostics (TCB_TRACE): %globaltimer at phase boundaries, first unit only.
 __device__ __forceinline__ void trace_mark(const Params& p, int slot, bool leader) {
   if (p.trace != nullptr && leader) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[blockIdx.x * 8 + slot] = t;
+    p.trace[blockIdx.x * 32 + slot] = t;
   }
 }
 __device__ __forceinline__ void consumer_sync() {
@@ -402,7 +435,8 @@ __device__ __forceinline__ void store_tile(const double (&acc)[8][4][2], double*
 template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA, bool SPLITK>
 __global__ void __launch_bounds__(NTHREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB) {
+                      const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC) {
   // Staged epilogue (TMA, no split-K): consumers dump the accumulator tile into
   // shared memory and go straight on to the next tile's main loop; producer
   // warps 1-3 apply alpha/beta and write C from there, overlapped with DMMA.
@@ -431,11 +465,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(empty0 + 8 * s, NCW);
     }
     mbar_init(stg_full, CTHREADS);
-    mbar_init(stg_empty, PTHREADS - 32);
+    mbar_init(stg_empty, p.c_tma ? 1 : PTHREADS - 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (USE_TMA) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      if (STAGED && p.c_tma)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
     }
   }
   __syncthreads();
@@ -447,6 +483,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int stid = tid - 32;  // 0..95
       const int swarp = stid >> 5, slane = stid & 31;
       uint32_t t = 0;
+      if (p.c_tma) {
+        // one thread: a TMA tensor store per tile straight from the staging
+        // buffer (no register traffic, clipped at the C edges)
+        if (stid != 0) return;
+        const uint32_t stg = smem_u32(staging);
+#pragma unroll 1
+        for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++t) {
+          const Unit un = decode_unit(p, u);
+          int c[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            const int src = p.pc.src[d];
+            unsigned v = src == 0 ? static_cast<unsigned>(un.tm * BM)
+                                  : (src == 1 ? static_cast<unsigned>(un.tn * BN)
+                                              : (src == 2 ? un.batch : 0u));
+            c[d] = static_cast<int>(prog_coord(p.pc, d, v));
+          }
+          mbar_wait(stg_full, t & 1);
+          tma_store5(&tmC, stg, c[0], c[1], c[2], c[3], c[4]);
+          bulk_wait_read();  // staging may be overwritten once read
+          mbar_arrive(stg_empty);
+        }
+        bulk_wait_all();
+        return;
+      }
 #pragma unroll 1
       for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++t) {
         const Unit un = decode_unit(p, u);
@@ -473,16 +534,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
         for (int n = swarp; n < BN; n += 3) {
           const int64_t coff = s_col[n];
-          const uint32_t sw = ((n >> 1) & 1) << 3;
           double v[BM / 32];
           int64_t roff[BM / 32];
 #pragma unroll
           for (int j = 0; j < BM / 32; ++j) {
             const int m = slane + 32 * j;
             roff[j] = s_row[m];
-            v[j] = staging[n * BM + (m ^ sw)];
+            v[j] = lds64(smem_u32(staging) + stage_off(m, n));
           }
-          if (coff < 0) continue;
+            if (coff < 0 || (p.diag & 1)) continue;
 #pragma unroll
           for (int j = 0; j < BM / 32; ++j) {
             if (roff[j] < 0) continue;
@@ -554,6 +614,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int kb = kb0; kb < kb1; ++kb) {
       const uint32_t stage = gcons % NST;
       mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
+      if (kb == kb0 && tcount > 0 && tcount <= 8)
+        trace_mark(p, 10 + 3 * (static_cast<int>(tcount) - 1), tl);
       if (gcons == 0) trace_mark(p, 1, tl);
       if (gcons == 8) trace_mark(p, 7, tl);
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
@@ -588,6 +650,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
     // ------------------------------ epilogue ------------------------------
     if (tcount == 0) trace_mark(p, 2, tl);
+    if (tcount < 8) trace_mark(p, 8 + 3 * static_cast<int>(tcount), tl);
     if constexpr (STAGED) {
       // hand the tile to the storers: wait until they drained the previous one,
       // write the raw accumulators ([n][m] with a bank swizzle on m), arrive.
@@ -601,16 +664,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
       }
       mbar_wait(stg_empty, (tcount & 1) ^ 1);
-      const uint32_t sw = (q & 1) << 3;  // ((n >> 1) & 1) << 3 for this thread's columns
+      const uint32_t stg = smem_u32(staging);
 #pragma unroll
       for (int im = 0; im < 8; ++im)
 #pragma unroll
         for (int in = 0; in < 4; ++in)
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj)
-            staging[(wn * 32 + in * 8 + 2 * q + jj) * BM + ((wm * 64 + im * 8 + r) ^ sw)] =
-                acc[im][in][jj];
+          for (int jj = 0; jj < 2; ++jj) {
+            const uint32_t a = stg + stage_off(wm * 64 + im * 8 + r, wn * 32 + in * 8 + 2 * q + jj);
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(acc[im][in][jj]) : "memory");
+          }
+      fence_proxy_async_smem();  // the TMA store reads these through the async proxy
       mbar_arrive(stg_full);
+      if (tcount < 8) trace_mark(p, 9 + 3 * static_cast<int>(tcount), tl);
       continue;
     }
     // Output offsets of this tile's 128 rows and 128 columns, decoded once
@@ -821,29 +887,9 @@ OperandGroups groups_of(const tcb_gemm_desc& d) {
 }
 bool has_groups(const tcb_gemm_desc& d) { return d.g_m > 0 || d.g_n > 0 || d.g_k > 0; }
 
-// Build the tensor map of one operand and its coordinate program.
-//   K-major:  [k inner: box 16] [outer: box spanning 128 indices] ...
-//   MN-major: [outer % 16: box 16] [k inner: box 16] [outer / 16: box spanning
-//             the 8 16-row chunks of the tile] ...
-// then the remaining sub-indices (box 1) and the batch dims with a non-zero
-// stride (box 1). A span may cover a whole sub-index whose extent divides it
-// and continue into the next one; span boundaries never cut a box row, so
-// inner extents of multi-index groups must be multiples of 16 (and of 128 /
-// divisors of 128 where they are spanned). One TMA instruction then loads an
-// operand's whole stage. MN-major operands with an outer extent that is not a
-// multiple of 16 (plain descriptors only) use eight 16x16 boxes instead.
-// Returns false with `why` set when TMA cannot describe the operand; plain
-// descriptors then fall back to cp.async.
-bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
-              const Group& outer, const Group& kg, const tcb_gemm_desc& d, const int64_t* bstr,
-              const char** why) {
-  auto fail = [&](const char* w) {
-    *why = w;
-    return false;
-  };
-  auto fn = encode_fn();
-  if (!fn) return fail("tensor-map encoder unavailable");
-  if (reinterpret_cast<uintptr_t>(base) % 16) return fail("operand not 16-byte aligned");
+// Accumulates the dimensions of one 5-D tensor map and its coordinate
+// program (see MapProg), then encodes it.
+struct MapBuilder {
   struct Dim {
     int64_t ext, str;
     uint32_t box;
@@ -852,14 +898,17 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
   };
   Dim dims[16];
   int r = 0;
-  auto push = [&](int64_t ext, int64_t str, uint32_t box, int src, int64_t div, int64_t mod) {
+  const char* err = nullptr;
+
+  void push(int64_t ext, int64_t str, uint32_t box, int src, int64_t div, int64_t mod) {
     if (r < 16) dims[r] = Dim{ext, str, box, src, div, mod};
     ++r;
-  };
-  // Sub-indices [from, n) of group g (index value = source / div0), the
-  // first `span` values of each tile covered by boxes; returns the next div.
-  auto push_span = [&](const Group& g, int from, int64_t span, int src, int64_t div0,
-                       const char** err) -> bool {
+  }
+  // Sub-indices [from, n) of group g (index value = source / div0): the first
+  // `span` values of each tile are covered by boxes — the whole first
+  // sub-index if its extent divides the span (then into the next one), else a
+  // span-sized box inside it; the remaining sub-indices get box 1.
+  bool push_span(const Group& g, int from, int64_t span, int src, int64_t div0) {
     const int n = g.n - from;
     const int64_t e0 = g.ext[from];
     int used = 1;
@@ -870,7 +919,7 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
     } else if (span % e0 == 0) {
       const int64_t e1 = g.ext[from + 1], b1 = span / e0;
       if (n > 2 && e1 % b1) {
-        *err = "second extent of a group does not tile the box";
+        err = "second extent of a group does not tile the box";
         return false;
       }
       push(e0, g.str[from], static_cast<uint32_t>(e0), src, div, e0);
@@ -878,7 +927,7 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
       div *= e0 * e1;
       used = 2;
     } else {
-      *err = "inner extent of a group does not tile the box";
+      err = "inner extent of a group does not tile the box";
       return false;
     }
     for (int j = from + used; j < g.n; ++j) {
@@ -886,31 +935,90 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
       div *= g.ext[j];
     }
     return true;
-  };
-  auto push_rest = [&](const Group& g, int src) {
+  }
+  // sub-indices 1.. of g, box 1
+  void push_rest(const Group& g, int src) {
     int64_t div = g.ext[0];
     for (int j = 1; j < g.n; ++j) {
       push(g.ext[j], g.str[j], 1, src, div, j + 1 < g.n ? g.ext[j] : 0);
       div *= g.ext[j];
     }
-  };
-  auto push_batch = [&]() {
+  }
+  // batch dims with a non-zero stride in this tensor, box 1
+  void push_batch(const tcb_gemm_desc& d, const int64_t* bstr) {
     int64_t div = 1;
     for (int i = 0; i < d.nbatch; ++i) {
       if (bstr[i] != 0 && d.bat_ext[i] > 1) push(d.bat_ext[i], bstr[i], 1, 2, div, d.bat_ext[i]);
       div *= d.bat_ext[i];
     }
+  }
+  // Encode (always 5 dims, so the kernel issues a single instruction form,
+  // cp.async.bulk.tensor.5d, whatever the rank) and fill the program.
+  bool encode(CUtensorMap* map, MapProg* prog, const double* base) {
+    auto fn = encode_fn();
+    if (!fn) return fail("tensor-map encoder unavailable");
+    if (reinterpret_cast<uintptr_t>(base) % 16) return fail("base not 16-byte aligned");
+    if (r > 5) return fail("more than 5 tensor-map dimensions");
+    cuuint64_t gdim[5], gstr[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    for (int i = 0; i < 5; ++i) {
+      const Dim x = i < r ? dims[i] : Dim{1, 2, 1, 3, 1, 0};
+      if (x.ext >= (1LL << 31) || x.div >= (1LL << 32) || x.mod >= (1LL << 32))
+        return fail("extent above 2^31");
+      gdim[i] = static_cast<cuuint64_t>(x.ext);
+      box[i] = x.box;
+      if (i > 0) {
+        const int64_t st = x.ext > 1 ? x.str : 2;  // extent-1 dims: any legal stride
+        if (st <= 0 || st % 2 || st * 8 >= (1LL << 40))
+          return fail("stride not a positive multiple of 16 bytes");
+        gstr[i - 1] = static_cast<cuuint64_t>(st * 8);
+      }
+      prog->src[i] = x.src;
+      prog->div[i] = static_cast<unsigned>(x.div);
+      prog->mod[i] = static_cast<unsigned>(x.mod);
+    }
+    const CUresult res =
+        fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), gdim, gstr, box,
+           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS) return fail("tensor-map encoding rejected");
+    return true;
+  }
+  bool fail(const char* w) {
+    err = w;
+    return false;
+  }
+};
+
+// Build the tensor map of one operand and its coordinate program.
+//   K-major:  [k inner: box 16] [outer: box spanning 128 indices] ...
+//   MN-major: [outer % 16: box 16] [k inner: box 16] [outer / 16: box spanning
+//             the 8 16-row chunks of the tile] ...
+// then the remaining sub-indices (box 1) and the batch dims with a non-zero
+// stride (box 1). Span boundaries never cut a box row, so inner extents of
+// multi-index groups must be multiples of 16 (and of 128 / divisors of 128
+// where they are spanned). One TMA instruction then loads an operand's whole
+// stage. MN-major operands with an outer extent that is not a multiple of 16
+// (plain descriptors only) use eight 16x16 boxes instead. Returns false with
+// `why` set when TMA cannot describe the operand; plain descriptors then fall
+// back to cp.async.
+bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
+              const Group& outer, const Group& kg, const tcb_gemm_desc& d, const int64_t* bstr,
+              const char** why) {
+  MapBuilder mb;
+  auto fail = [&](const char* w) {
+    *why = w;
+    return false;
   };
   const Group& lead = kmajor ? kg : outer;
   if (lead.str[0] != 1 && lead.ext[0] > 1) return fail("no unit-stride inner index");
   if (kg.n > 1 && kg.ext[0] % 16) return fail("inner extent of a k group not a multiple of 16");
-  const char* err = nullptr;
   prog->nbox = 1;
   if (kmajor) {
-    push(kg.ext[0], 1, 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
-    if (!push_span(outer, 0, BN, 0, 1, &err)) return fail(err);
-    push_rest(kg, 1);
-    push_batch();
+    mb.push(kg.ext[0], 1, 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
+    if (!mb.push_span(outer, 0, BN, 0, 1)) return fail(mb.err);
+    mb.push_rest(kg, 1);
+    mb.push_batch(d, bstr);
   } else {
     const int64_t e0 = outer.ext[0];
     bool spanned = false;
@@ -921,56 +1029,66 @@ bool make_map(CUtensorMap* map, MapProg* prog, const double* base, bool kmajor,
       Group hi = outer;
       hi.ext[0] = e0 / 16;
       hi.str[0] = 16 * outer.str[0];
-      int from = (hi.ext[0] == 1 && hi.n > 1) ? 1 : 0;
-      push(16, 1, 16, 0, 1, 16);
-      push(kg.ext[0], kg.str[0], 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
-      if (!push_span(hi, from, BM / 16, 0, 16, &err)) return fail(err);
-      push_rest(kg, 1);
-      push_batch();
-      spanned = r <= 5;
+      const int from = (hi.ext[0] == 1 && hi.n > 1) ? 1 : 0;
+      mb.push(16, 1, 16, 0, 1, 16);
+      mb.push(kg.ext[0], kg.str[0], 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
+      if (!mb.push_span(hi, from, BM / 16, 0, 16)) return fail(mb.err);
+      mb.push_rest(kg, 1);
+      mb.push_batch(d, bstr);
+      spanned = mb.r <= 5;
       if (!spanned && outer.n > 1) return fail("more than 5 tensor-map dimensions");
     } else if (outer.n > 1) {
       return fail("inner extent of a unit-stride group not a multiple of 16");
     }
     if (!spanned) {  // plain operand: eight 16 x 16 boxes per stage
-      r = 0;
+      mb.r = 0;
       prog->nbox = BM / 16;
-      push(e0, 1, 16, 0, 1, 0);
-      push(kg.ext[0], kg.str[0], 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
-      push_rest(kg, 1);
-      push_batch();
+      mb.push(e0, 1, 16, 0, 1, 0);
+      mb.push(kg.ext[0], kg.str[0], 16, 1, 1, kg.n > 1 ? kg.ext[0] : 0);
+      mb.push_rest(kg, 1);
+      mb.push_batch(d, bstr);
     }
   }
-  if (r > 5) return fail("more than 5 tensor-map dimensions");
-  cuuint64_t gdim[5], gstr[4];
-  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
-  for (int i = 0; i < 5; ++i) {
-    const Dim x = i < r ? dims[i] : Dim{1, 2, 1, 3, 1, 0};
-    if (x.ext >= (1LL << 31) || x.div >= (1LL << 32) || x.mod >= (1LL << 32))
-      return fail("extent above 2^31");
-    gdim[i] = static_cast<cuuint64_t>(x.ext);
-    box[i] = x.box;
-    if (i > 0) {
-      const int64_t st = x.ext > 1 ? x.str : 2;  // extent-1 dims: any legal stride
-      if (st <= 0 || st % 2 || st * 8 >= (1LL << 40))
-        return fail("stride not a positive multiple of 16 bytes");
-      gstr[i - 1] = static_cast<cuuint64_t>(st * 8);
-    }
-    prog->src[i] = x.src;
-    prog->div[i] = static_cast<unsigned>(x.div);
-    prog->mod[i] = static_cast<unsigned>(x.mod);
-  }
+  if (!mb.encode(map, prog, base)) return fail(mb.err);
   prog->kdim = -1;
   if (kg.n == 1)
     for (int i = 0; i < 5; ++i)
       if (prog->src[i] == 1) prog->kdim = i;
-  // Always 5 dims, so the kernel issues a single instruction form
-  // (cp.async.bulk.tensor.5d) whatever the operand's rank.
-  const CUresult res =
-      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), gdim, gstr, box, estr,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (res != CUDA_SUCCESS) return fail("tensor-map encoding rejected");
+  return true;
+}
+
+// Tensor map of the output tile for the TMA-store epilogue: [m % 16: box 16]
+// [n: box spanning 128] [m / 16: box spanning the 8 chunks] [rest] [batch],
+// coordinate sources 0 = m origin, 1 = n origin, 2 = batch index. Its smem
+// image (8 boxes of [n 128][m 16], 128B-swizzled) is the staging layout.
+// Needs the output rows' inner sub-index unit-stride with an extent that is
+// a multiple of 16 (so a box never writes past a row run).
+bool make_cmap(CUtensorMap* map, MapProg* prog, double* C, const tcb_gemm_desc& d,
+               const char** why) {
+  Group row, col;
+  row.many(d.c_nrow, d.c_row_ext, d.c_row_str);
+  col.many(d.c_ncol, d.c_col_ext, d.c_col_str);
+  if (row.str[0] != 1 || row.ext[0] % 16) {
+    *why = "output rows not unit-stride in runs of 16";
+    return false;
+  }
+  MapBuilder mb;
+  Group hi = row;
+  hi.ext[0] = row.ext[0] / 16;
+  hi.str[0] = 16;
+  const int from = (hi.ext[0] == 1 && hi.n > 1) ? 1 : 0;
+  mb.push(16, 1, 16, 0, 1, 16);
+  bool ok = mb.push_span(col, 0, BN, 1, 1) && mb.push_span(hi, from, BM / 16, 0, 16);
+  if (ok) {
+    mb.push_batch(d, d.bat_sc);
+    ok = mb.encode(map, prog, C);
+  }
+  if (!ok) {
+    *why = mb.err;
+    return false;
+  }
+  prog->nbox = 1;
+  prog->kdim = -1;
   return true;
 }
 
@@ -981,8 +1099,8 @@ bool kmajor_of(const Group& outer, const Group& kg) {
 }
 
 template <bool AK, bool BK_, bool TMA>
-cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap& tb, int grid,
-                       cudaStream_t s) {
+cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap& tb,
+                       const CUtensorMap& tc, int grid, cudaStream_t s) {
   const bool split = p.splits > 1;
   auto kern = split ? dgemm_dmma_kernel<AK, BK_, TMA, true> : dgemm_dmma_kernel<AK, BK_, TMA, false>;
   const int smem = split ? smem_bytes<false>() : smem_bytes<TMA>();
@@ -1007,7 +1125,7 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
   attr[0].val.cooperative = p.splits > 1 ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p, ta, tb);
+  return cudaLaunchKernelEx(&cfg, kern, p, ta, tb, tc);
 }
 
 }  // namespace
@@ -1142,27 +1260,38 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
                    make_map(&tb, &p.pb, B, b_k, g.bn, g.bk, d, d.bat_sb, &why);
   // index groups are read through the tensor maps only
   if (!tma && has_groups(d)) return set_error(TCB_EUNSUPPORTED, std::string("gemm: index groups: ") + why);
+  // staged epilogue: C by TMA store when beta == 0 and the map describes C
+  CUtensorMap tc;
+  std::memset(&tc, 0, sizeof tc);
+  static const bool no_cstore = getenv("TCB_NO_CSTORE") != nullptr;  // diagnostics
+  p.c_tma = 0;
+  if (tma && splits == 1 && d.beta == 0.0 && !no_cstore) {
+    const char* cwhy = nullptr;
+    p.c_tma = make_cmap(&tc, &p.pc, C, d, &cwhy) ? 1 : 0;
+  }
 
   const int grid = static_cast<int>(std::min<int64_t>(p.units, sms));
   // TCB_TRACE=<file>: append per-CTA phase timestamps of this launch (diagnostics)
   static const char* trace_path = getenv("TCB_TRACE");
   unsigned long long* trace = nullptr;
   if (trace_path) {
-    TCB_CUDA(cudaMalloc(&trace, grid * 8 * sizeof(unsigned long long)));
-    TCB_CUDA(cudaMemsetAsync(trace, 0, grid * 8 * sizeof(unsigned long long), st.stream));
+    TCB_CUDA(cudaMalloc(&trace, grid * 32 * sizeof(unsigned long long)));
+    TCB_CUDA(cudaMemsetAsync(trace, 0, grid * 32 * sizeof(unsigned long long), st.stream));
   }
   p.trace = trace;
+  static const int diag = getenv("TCB_DIAG") ? atoi(getenv("TCB_DIAG")) : 0;
+  p.diag = diag;
   cudaError_t e;
   if (tma) {
-    if (a_k && b_k) e = launch_one<true, true, true>(p, ta, tb, grid, st.stream);
-    else if (a_k) e = launch_one<true, false, true>(p, ta, tb, grid, st.stream);
-    else if (b_k) e = launch_one<false, true, true>(p, ta, tb, grid, st.stream);
-    else e = launch_one<false, false, true>(p, ta, tb, grid, st.stream);
+    if (a_k && b_k) e = launch_one<true, true, true>(p, ta, tb, tc, grid, st.stream);
+    else if (a_k) e = launch_one<true, false, true>(p, ta, tb, tc, grid, st.stream);
+    else if (b_k) e = launch_one<false, true, true>(p, ta, tb, tc, grid, st.stream);
+    else e = launch_one<false, false, true>(p, ta, tb, tc, grid, st.stream);
   } else {
-    if (a_k && b_k) e = launch_one<true, true, false>(p, ta, tb, grid, st.stream);
-    else if (a_k) e = launch_one<true, false, false>(p, ta, tb, grid, st.stream);
-    else if (b_k) e = launch_one<false, true, false>(p, ta, tb, grid, st.stream);
-    else e = launch_one<false, false, false>(p, ta, tb, grid, st.stream);
+    if (a_k && b_k) e = launch_one<true, true, false>(p, ta, tb, tc, grid, st.stream);
+    else if (a_k) e = launch_one<true, false, false>(p, ta, tb, tc, grid, st.stream);
+    else if (b_k) e = launch_one<false, true, false>(p, ta, tb, tc, grid, st.stream);
+    else e = launch_one<false, false, false>(p, ta, tb, tc, grid, st.stream);
   }
   if (e != cudaSuccess) {
     st.last_splits = 0;
@@ -1170,7 +1299,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
   ++st.launches;
   if (trace) {
-    std::vector<unsigned long long> h(static_cast<size_t>(grid) * 8);
+    std::vector<unsigned long long> h(static_cast<size_t>(grid) * 32);
     TCB_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st.stream));
     TCB_CUDA(cudaStreamSynchronize(st.stream));
     cudaFree(trace);

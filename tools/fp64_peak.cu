@@ -25,6 +25,29 @@ __global__ void dmma_m8n8k4(double* out, int iters) {
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
+// NACC accumulators, each updated CHAIN times in a row (k-chained issue order)
+template <int NACC, int CHAIN>
+__global__ void dmma_chain(double* out, int iters) {
+  double a[CHAIN], b[CHAIN];
+#pragma unroll
+  for (int i = 0; i < CHAIN; ++i) { a[i] = 1.0 + (threadIdx.x + i) * 1e-9; b[i] = 1.0 - i * 1e-9; }
+  double c[NACC][2];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) { c[i][0] = 0; c[i][1] = 0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i)
+#pragma unroll
+      for (int k = 0; k < CHAIN; ++k)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a[k]), "d"(b[k]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
 template <int NACC>
 __global__ void dmma_m16n8k16(double* out, int iters) {
   double a[8], b[4];
@@ -104,6 +127,12 @@ int main() {
     run("dmma_m8n8k4_acc16", dmma_m8n8k4<16>, 128, bps, it, 16 * 16.0, out, nsm);
   run("dmma_m8n8k4_acc4_256t", dmma_m8n8k4<4>, 256, 2, it, 4 * 16.0, out, nsm);
   run("dmma_m8n8k4_acc1_1024t", dmma_m8n8k4<1>, 1024, 1, it, 1 * 16.0, out, nsm);
+  for (int bps : {1, 2}) {
+    run("dmma_m8n8k4_acc8_chain2", dmma_chain<8, 2>, 128, bps, it / 2, 16 * 16.0, out, nsm);
+    run("dmma_m8n8k4_acc8_chain4", dmma_chain<8, 4>, 128, bps, it / 4, 32 * 16.0, out, nsm);
+    run("dmma_m8n8k4_acc16_chain4", dmma_chain<16, 4>, 128, bps, it / 4, 64 * 16.0, out, nsm);
+    run("dmma_m8n8k4_acc32_chain1", dmma_chain<32, 1>, 128, bps, it / 4, 32 * 16.0, out, nsm);
+  }
   // m16n8k16: 16*8*16 = 2048 FMA per warp -> 128 flop per thread
   for (int bps : {1, 2, 4})
     run("dmma_m16n8k16_acc4", dmma_m16n8k16<4>, 128, bps, it / 4, 4 * 128.0, out, nsm);

@@ -8,11 +8,20 @@ names = ["start->first data", "mainloop (first unit)", "partials written", "all 
 for line in open(sys.argv[1]):
     d = json.loads(line)
     g = d["grid"]
-    t = [d["t"][i * 8:(i + 1) * 8] for i in range(g)]
+    w = len(d["t"]) // g  # slots per CTA (8, or 16 with per-tile marks)
+    t = [d["t"][i * w:(i + 1) * w] for i in range(g)]
     t0 = min(x[0] for x in t if x[0])
     print(f"m={d['m']} n={d['n']} k={d['k']} splits={d['splits']} grid={g}")
     ends = [max(x) for x in t]
-    print(f"  kernel span (first CTA start -> last mark): {(max(ends) - t0) / 1e3:.1f} us")
+    if w == 32:  # slots 8+3t: tile t mainloop end, 9+3t: epilogue handed off, 10+3t: next data
+        med = lambda v: statistics.median(v) if v else float("nan")
+        for j in range(0, 7):
+            a, b, c, nxt = (8 + 3 * j, 9 + 3 * j, 10 + 3 * j, 8 + 3 * (j + 1))
+            epi = [(x[b] - x[a]) / 1e3 for x in t if x[a] and x[b]]
+            gap = [(x[c] - x[b]) / 1e3 for x in t if x[b] and x[c]]
+            loop = [(x[nxt] - x[c]) / 1e3 for x in t if x[c] and x[nxt]]
+            print(f"  tile {j + 1}: epilogue {med(epi):6.2f}  wait first data {med(gap):6.2f}  "
+                  f"mainloop {med(loop):7.2f} us (median over CTAs)")
     starts = [x[0] - t0 for x in t]
     print(f"  CTA start skew: median {statistics.median(starts)/1e3:.2f} max {max(starts)/1e3:.2f} us")
     r1 = [(x[7] - x[1]) / 8e3 for x in t if x[7] and x[1]]
