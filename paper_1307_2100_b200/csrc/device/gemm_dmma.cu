@@ -600,9 +600,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   trace_mark(p, 0, tl);
 #pragma unroll 1
   for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++tcount) {
-    const Unit un = decode_unit(p, u);
-    const int kb0 = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
-    const int kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
+    // the staged epilogue (never split) needs no unit decode on the consumers
+    Unit un{};
+    int kb0 = 0, kb1 = p.kblocks;
+    if constexpr (!STAGED) {
+      un = decode_unit(p, u);
+      kb0 = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
+      kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
+    }
 
     double acc[8][4][2];
 #pragma unroll
