@@ -123,19 +123,19 @@ __global__ void __launch_bounds__(256) gemv_kmajor(GvParams p) {
 // Row-contiguous matrix, 16 warps per block. A warp covers RL*VR consecutive
 // rows x G = 32/RL consecutive columns, where RL (<= 32) is the number of lanes
 // along rows (fewer than 32 when the matrix has few rows: short-wide matrices
-// still get 256-byte warp accesses). Lane (r, c) owns rows r*VR..r*VR+VR-1
+// still get 128-256-byte warp accesses). Lane (r, c) owns rows r*VR..r*VR+VR-1
 // (16-byte loads when VR == 2) and, with the warp index ty, the k-lanes
-// c + G*ty + 16G*j of the canonical 64-lane order; the next 64-column step's
-// loads are issued before the current step's FMAs. Lane sums meet in shared
-// memory and are combined with the same tree as gemv_kmajor.
-template <int VR>
-__global__ void __launch_bounds__(512) gemv_omajor(GvParams p, int RL) {
+// c + G*ty + 16G*j (j < NJ = 4/G) of the canonical 64-lane order. The loads
+// of DEPTH 64-column steps are in flight at once (DEPTH*NJ*VR doubles per
+// thread). Lane sums meet in shared memory and are combined with the same
+// tree as gemv_kmajor.
+template <int VR, int G>
+__global__ void __launch_bounds__(512) gemv_omajor(GvParams p) {
+  constexpr int RL = 32 / G, NJ = 4 / G, DEPTH = 4;
   __shared__ double red[64][64 + 1];
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int G = 32 / RL;            // columns per warp access
-  const int NJ = 4 / G;             // k-lanes per thread (16 warps; G divides 4)
   const int r = lane % RL, c = lane / RL;
-  const int rows_per_tile = RL * VR;
+  constexpr int rows_per_tile = RL * VR;
   const int64_t rblocks = (p.rows + rows_per_tile - 1) / rows_per_tile;
   const int64_t items = p.batch * rblocks * p.splits;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -146,57 +146,50 @@ __global__ void __launch_bounds__(512) gemv_omajor(GvParams p, int RL) {
     gv_batch(p, b, om, ov, oy);
     const int64_t o = rb * rows_per_tile + r * VR;  // first row of this lane
     const int64_t k0 = s * p.chunk, k1 = min(p.K, k0 + p.chunk);
-    double acc[4][VR];
+    double acc[NJ][VR];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int v = 0; v < VR; ++v) acc[j][v] = 0.0;
-    const bool row_ok = o < p.rows;
-    if (row_ok) {
+    if (o < p.rows) {
       const double* mcol = p.M + om + o * p.so;
       const double* vec = p.v + ov;
-      // software-pipelined: the next 64-column step's loads are in flight
-      // while the current step's FMAs run (16 loads per thread outstanding)
-      double a[4][VR], x[4];
-      auto load = [&](int64_t kb, double (&aa)[4][VR], double (&xx)[4]) {
+      const int kl = c + G * ty;  // this thread's first k-lane
+#pragma unroll 1
+      for (int64_t kb = k0; kb < k1; kb += 64 * DEPTH) {
+        double a[DEPTH][NJ][VR], x[DEPTH][NJ];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t k = kb + c + G * (ty + 16 * j);
-          const bool ok = j < NJ && k < k1;
-          xx[j] = ok ? __ldg(vec + k * p.sv) : 0.0;
-          if (VR == 2) {
-            const double2 t = ok ? __ldcs(reinterpret_cast<const double2*>(mcol + k * p.sk))
-                                 : make_double2(0.0, 0.0);
-            aa[j][0] = t.x;
-            aa[j][VR - 1] = t.y;
-          } else {
-            aa[j][0] = ok ? __ldcs(mcol + k * p.sk) : 0.0;
+        for (int d = 0; d < DEPTH; ++d)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            const int64_t k = kb + 64 * d + kl + 16 * G * j;
+            const bool ok = k < k1;
+            x[d][j] = ok ? __ldg(vec + k * p.sv) : 0.0;
+            if (VR == 2) {
+              const double2 t = ok ? __ldcs(reinterpret_cast<const double2*>(mcol + k * p.sk))
+                                   : make_double2(0.0, 0.0);
+              a[d][j][0] = t.x;
+              a[d][j][VR - 1] = t.y;
+            } else {
+              a[d][j][0] = ok ? __ldcs(mcol + k * p.sk) : 0.0;
+            }
           }
-        }
-      };
-      load(k0, a, x);
-      for (int64_t kb = k0; kb < k1; kb += 64) {
-        double an[4][VR], xn[4];
-        if (kb + 64 < k1) load(kb + 64, an, xn);
+        // in increasing k per k-lane; out-of-range terms are skipped (not
+        // added as zeros) so the FMA chain matches the canonical order exactly
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < NJ && kb + c + G * (ty + 16 * j) < k1)
+        for (int d = 0; d < DEPTH; ++d)
 #pragma unroll
-            for (int v = 0; v < VR; ++v) acc[j][v] = fma(a[j][v], x[j], acc[j][v]);
+          for (int j = 0; j < NJ; ++j)
+            if (kb + 64 * d + kl + 16 * G * j < k1)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          x[j] = xn[j];
-#pragma unroll
-          for (int v = 0; v < VR; ++v) a[j][v] = an[j][v];
-        }
+              for (int v = 0; v < VR; ++v) acc[j][v] = fma(a[d][j][v], x[d][j], acc[j][v]);
       }
     }
     // red[lambda][row in tile]
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < NJ)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int v = 0; v < VR; ++v) red[c + G * (ty + 16 * j)][r * VR + v] = acc[j][v];
+      for (int v = 0; v < VR; ++v) red[c + G * (ty + 16 * j)][r * VR + v] = acc[j][v];
     __syncthreads();
     for (int rr = threadIdx.x; rr < rows_per_tile; rr += blockDim.x) {
       const int64_t orow = rb * rows_per_tile + rr;
@@ -295,7 +288,8 @@ int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double
   // Chunking depends only on (batch*rows, K) — never on the kernel — and
   // chunks are multiples of 64, so the summation order is layout-free.
   const int64_t rows_total = p.batch * p.rows;
-  const int64_t target = static_cast<int64_t>(sms) * 256;
+  // enough (row, chunk) items for several waves of either kernel
+  const int64_t target = static_cast<int64_t>(sms) * 2048;
   int64_t splits = 1;
   if (rows_total < target)
     splits = std::min<int64_t>((target + rows_total - 1) / rows_total,
@@ -333,14 +327,21 @@ int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double
     int RL = 32;
     while (RL > 1 && RL / 2 >= p.rows) RL /= 2;
     if (RL < 8) RL = 8;  // G = 32/RL must divide 4
-    bool vr2 = RL == 32 && p.rows >= 64 && p.rows % 2 == 0 && p.so == 1 && p.sk % 2 == 0 &&
+    bool vr2 = p.rows % 2 == 0 && p.so == 1 && p.sk % 2 == 0 &&
                reinterpret_cast<uintptr_t>(p.M) % 16 == 0;
     for (int i = 0; i < d.nbatch && vr2; ++i) vr2 = p.bat_sm[i] % 2 == 0;
+    // two rows per lane: half the lanes along rows when that still covers them
+    if (vr2 && p.rows < 2 * RL) {
+      if (RL > 8) RL /= 2;
+      else vr2 = false;
+    }
+    const int g = 32 / RL;
     const int per_tile = RL * (vr2 ? 2 : 1);
     const int64_t items = p.batch * ((p.rows + per_tile - 1) / per_tile) * splits;
     const int blocks = static_cast<int>(std::min<int64_t>(items, sms * 8LL));
-    if (vr2) gemv_omajor<2><<<blocks, 512, 0, st.stream>>>(p, RL);
-    else gemv_omajor<1><<<blocks, 512, 0, st.stream>>>(p, RL);
+    auto kern = vr2 ? (g == 1 ? gemv_omajor<2, 1> : g == 2 ? gemv_omajor<2, 2> : gemv_omajor<2, 4>)
+                    : (g == 1 ? gemv_omajor<1, 1> : g == 2 ? gemv_omajor<1, 2> : gemv_omajor<1, 4>);
+    kern<<<blocks, 512, 0, st.stream>>>(p);
   }
   TCB_LAUNCHED();
   ++launches;
