@@ -129,9 +129,23 @@ __global__ void __launch_bounds__(256) gemv_kmajor(GvParams p) {
 // of DEPTH 64-column steps are in flight at once (DEPTH*NJ*VR doubles per
 // thread). Lane sums meet in shared memory and are combined with the same
 // tree as gemv_kmajor.
+// The canonical combination of the 64 k-lane sums of one row (column rr of
+// red): pairs (2j, 2j+1), then the xor tree of gemv_kmajor's shuffles —
+// T(lo, step, n) = T(lo, 2 step, n/2) + T(lo + step, 2 step, n/2) — evaluated
+// depth first so only ~log2(32) partial sums are live.
+template <int LO, int STEP, int N>
+__device__ __forceinline__ double lane_tree(const double (*red)[64 + 1], int rr) {
+  if constexpr (N == 1) {
+    return red[2 * LO][rr] + red[2 * LO + 1][rr];
+  } else {
+    const double a = lane_tree<LO, 2 * STEP, N / 2>(red, rr);
+    return a + lane_tree<LO + STEP, 2 * STEP, N / 2>(red, rr);
+  }
+}
+
 template <int VR, int G>
-__global__ void __launch_bounds__(512) gemv_omajor(GvParams p) {
-  constexpr int RL = 32 / G, NJ = 4 / G, DEPTH = 4;
+__global__ void __launch_bounds__(512, 2) gemv_omajor(GvParams p) {
+  constexpr int RL = 32 / G, NJ = 4 / G, DEPTH = 2;
   __shared__ double red[64][64 + 1];
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int r = lane % RL, c = lane / RL;
@@ -194,14 +208,7 @@ __global__ void __launch_bounds__(512) gemv_omajor(GvParams p) {
     for (int rr = threadIdx.x; rr < rows_per_tile; rr += blockDim.x) {
       const int64_t orow = rb * rows_per_tile + rr;
       if (orow >= p.rows) continue;
-      double l[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) l[i] = red[2 * i][rr] + red[2 * i + 1][rr];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-        for (int i = 0; i < off; ++i) l[i] = l[i] + l[i + off];
-      gv_store(p, b, orow, s, l[0]);
+      gv_store(p, b, orow, s, lane_tree<0, 1, 32>(red, rr));
     }
     __syncthreads();
   }
