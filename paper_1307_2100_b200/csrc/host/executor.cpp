@@ -360,9 +360,26 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
         label = -1;
   }
   if (label >= 0 && slabs <= 0) {
-    // auto: ~16 MB of streamed operand + output per slab, up to 64 slabs
+    // auto: ~16 MB of streamed operand + output per slab, up to 64 slabs, but
+    // no thinner than keeps the slab GEMM's 128x128 tiles as full as the
+    // whole contraction's (cfg4: 64 slabs of j would halve every tile)
     const std::int64_t bytes = ((on_left ? nl_ : nr_) + no_) * 8;
     slabs = static_cast<int>(std::min<std::int64_t>(64, bytes / (16LL << 20)));
+    const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
+    auto tile_eff = [](const DeviceRecipe& r) {
+      if (r.m == 1 || r.n == 1) return 1.0;  // GEMV / DOT: no tiles
+      const double pm = static_cast<double>((r.m + 127) / 128 * 128);
+      const double pn = static_cast<double>((r.n + 127) / 128 * 128);
+      return static_cast<double>(r.m) * static_cast<double>(r.n) / (pm * pn);
+    };
+    const double full = tile_eff(recipe_);
+    while (slabs >= 2) {
+      ValidatedContraction sv = v_;
+      sv.labels[static_cast<std::size_t>(label)].extent = std::max<std::int64_t>(1, E / slabs);
+      bool ok = groups_ok_;
+      if (tile_eff(lower_checked(sv, &ok)) >= 0.95 * full) break;
+      slabs = slabs > 8 ? slabs - slabs / 4 : slabs - 1;
+    }
   }
   int pinned_l = 0, pinned_r = 0, pinned_o = 0;
   tcb_host_is_pinned(left, &pinned_l);
