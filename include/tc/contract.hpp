@@ -427,6 +427,7 @@ class PreparedContraction {
   DeviceRecipe recipe_;
   ValidatedContraction v_;
   bool groups_ok_ = true;  // L4 allowed (cleared if the device refuses it)
+  int auto_slabs_ = -1;    // run_streamed's automatic slab count, once decided
   int device_ = 0;
   std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
   double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;

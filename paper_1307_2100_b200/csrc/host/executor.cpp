@@ -360,26 +360,33 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
         label = -1;
   }
   if (label >= 0 && slabs <= 0) {
-    // auto: ~16 MB of streamed operand + output per slab, up to 64 slabs, but
-    // no thinner than keeps the slab GEMM's 128x128 tiles as full as the
-    // whole contraction's (cfg4: 64 slabs of j would halve every tile)
-    const std::int64_t bytes = ((on_left ? nl_ : nr_) + no_) * 8;
-    slabs = static_cast<int>(std::min<std::int64_t>(64, bytes / (16LL << 20)));
-    const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
-    auto tile_eff = [](const DeviceRecipe& r) {
-      if (r.m == 1 || r.n == 1) return 1.0;  // GEMV / DOT: no tiles
-      const double pm = static_cast<double>((r.m + 127) / 128 * 128);
-      const double pn = static_cast<double>((r.n + 127) / 128 * 128);
-      return static_cast<double>(r.m) * static_cast<double>(r.n) / (pm * pn);
-    };
-    const double full = tile_eff(recipe_);
-    while (slabs >= 2) {
-      ValidatedContraction sv = v_;
-      sv.labels[static_cast<std::size_t>(label)].extent = std::max<std::int64_t>(1, E / slabs);
-      bool ok = groups_ok_;
-      if (tile_eff(lower_checked(sv, &ok)) >= 0.95 * full) break;
-      slabs = slabs > 8 ? slabs - slabs / 4 : slabs - 1;
+    // auto (decided once per prepared contraction): ~16 MB of streamed operand
+    // + output per slab, up to 64 slabs, but no thinner than keeps both slab
+    // sizes' GEMM tiles (128x128) as full as the whole contraction's — cfg4's
+    // 64 one-j slabs would leave every tile half empty
+    if (auto_slabs_ < 0) {
+      const std::int64_t bytes = ((on_left ? nl_ : nr_) + no_) * 8;
+      int want = static_cast<int>(std::min<std::int64_t>(64, bytes / (16LL << 20)));
+      const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
+      auto tile_eff = [&](std::int64_t e) {
+        ValidatedContraction sv = v_;
+        sv.labels[static_cast<std::size_t>(label)].extent = e;
+        bool ok = groups_ok_;
+        const DeviceRecipe r = lower_checked(sv, &ok);
+        if (r.m == 1 || r.n == 1) return 1.0;  // GEMV / DOT: no tiles
+        const double pm = static_cast<double>((r.m + 127) / 128 * 128);
+        const double pn = static_cast<double>((r.n + 127) / 128 * 128);
+        return static_cast<double>(r.m) * static_cast<double>(r.n) / (pm * pn);
+      };
+      const double full = tile_eff(E);
+      want = static_cast<int>(std::min<std::int64_t>(want, E));
+      for (; want >= 2; --want) {
+        const std::int64_t lo = E / want, hi = (E + want - 1) / want;
+        if (tile_eff(lo) >= 0.95 * full && (hi == lo || tile_eff(hi) >= 0.95 * full)) break;
+      }
+      auto_slabs_ = want;
     }
+    slabs = auto_slabs_;
   }
   int pinned_l = 0, pinned_r = 0, pinned_o = 0;
   tcb_host_is_pinned(left, &pinned_l);
