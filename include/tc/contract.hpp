@@ -1,13 +1,16 @@
 // tc:: — the reference's contraction API (/root/reference/proj/include/tc/*.hpp),
 // re-declared for the B200 engine so existing callers compile unchanged.
 // The per-topic headers tc/tensor.hpp, tc/expr.hpp, tc/planner.hpp,
-// tc/kernels.hpp and tc/executor.hpp include this file.
+// tc/kernels.hpp, tc/executor.hpp, tc/tensor_io.hpp and tc/bench.hpp include
+// this file.
 //
 // Everything here is host C++ (no CUDA types). Arithmetic goes to the device
 // through the C-ABI in tcb.h; see DESIGN.md for the lowering.
 #pragma once
 
 #include <cstdint>
+#include <iosfwd>
+#include <map>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -436,5 +439,56 @@ class PreparedContraction {
   struct Pipes;
   std::unique_ptr<Pipes> pipes_;  // streamed path: copy streams + events
 };
+
+
+// ---------------------------------------------------------------- tensor I/O
+// The reference's TENSOR v1 text format (include/tc/tensor_io.hpp:9-16,
+// src/tensor_io.cpp): header lines `TENSOR v1`, `name`, `rank`, `extents`,
+// `variance`, `layout colmajor`, then the values in storage order with 17
+// significant digits, eight per line. Byte-identical output; the engine
+// formats and parses large tensors in parallel blocks.
+void write_tensor(std::ostream& os, const Tensor& t);
+void write_tensor_file(const std::string& path, const Tensor& t);
+Tensor read_tensor(std::istream& is);
+Tensor read_tensor_file(const std::string& path);
+
+// ---------------------------------------------------------------- benchmark
+// The reference's benchmark sweep (include/tc/bench.hpp:13-51,
+// src/bench.cpp): built-in experiments square3d / cc4d / gr4d or a custom
+// expression, one row per (contraction, forced kernel, size), median of the
+// timed repetitions after one warm-up; backend "b200" runs each evaluation on
+// the device (ExecutionStats::wall_seconds, transfers included).
+struct BenchConfig {
+  std::string experiment = "square3d";  // square3d | cc4d | gr4d | custom
+  std::vector<std::int64_t> sizes;
+  std::vector<KernelKind> kernels;
+  std::string backend = "b200";
+  int repetitions = 5;
+  std::uint64_t seed = 1;
+  std::int64_t mem_cap_bytes = 4000000000;
+  bool verify_sample = false;
+  int workers = 1;
+  std::string custom_expr;
+  std::map<std::string, std::int64_t> custom_extents;
+};
+
+struct BenchRow {
+  std::string experiment;
+  std::string expression;
+  std::int64_t size = 0;
+  std::string kernel;
+  std::string backend;
+  int repetitions = 0;
+  double median_seconds = 0.0;
+  double gflops = 0.0;
+  std::int64_t packed_bytes = 0;
+  bool available = false;
+  bool verified_ok = true;  // true when sampling is off or the sample matched
+};
+
+std::vector<BenchRow> run_bench(const BenchConfig& config);
+/// Columns: experiment, expression, size, kernel, backend, repetitions,
+/// median_seconds, gflops, packed_bytes; unavailable kernels carry NA cells.
+void write_bench_csv(std::ostream& os, const std::vector<BenchRow>& rows);
 
 }  // namespace tc

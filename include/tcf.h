@@ -64,6 +64,25 @@ int tcf_device_ptrs(void* handle, void** left, void** right, void** out);
 int tcf_release(void* handle);
 const char* tcf_last_error(void);
 
+/* ---- TENSOR v1 text (tc::write_tensor / tc::read_tensor; reference
+ * include/tc/tensor_io.hpp:9-22) ----------------------------------------- */
+/* Text of Tensor::seeded_random(ext[0..rank), var ("+-" chars), seed, name). */
+int tcf_tensor_text(const int64_t* ext, int rank, const char* var, uint64_t seed,
+                    const char* name, char* buf, int64_t cap);
+/* Parse text: *n = element count, values into out (cap elements); the
+ * reference's messages on malformed input ("not a TENSOR v1 file", ...). */
+int tcf_read_tensor_text(const char* text, double* out, int64_t cap, int64_t* n, char* err,
+                         int64_t errcap);
+
+/* ---- benchmark sweep (tc::run_bench + tc::write_bench_csv; reference
+ * include/tc/bench.hpp:13-51) ----------------------------------------------
+ * sizes "150,200"; kernels "GEMM,COPY+GEMM,..."; custom_extents "a=3,b=4".
+ * CSV into csv; *verified = 1 when every sampled line matched. */
+int tcf_bench_csv(const char* experiment, const char* sizes, const char* kernels,
+                  const char* backend, int repetitions, uint64_t seed, int verify, int workers,
+                  const char* custom_expr, const char* custom_extents, char* csv, int64_t cap,
+                  int* verified);
+
 #ifdef __cplusplus
 }
 #endif

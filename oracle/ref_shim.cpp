@@ -17,6 +17,7 @@
 #include <string>
 
 #include "tc/executor.hpp"
+#include "tc/tensor_io.hpp"
 #include "tc/oracle.hpp"
 #include "tc/planner.hpp"
 
@@ -230,6 +231,43 @@ __attribute__((visibility("default"))) int ref_gemm(int ta, int tb, std::int64_t
                                                     char* err, std::int64_t errcap) {
   try {
     tc::make_reference_backend()->gemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errcap, 1);
+  }
+}
+
+// TENSOR v1 text of Tensor::seeded_random(ext, var, seed, name) through the
+// reference writer (src/tensor_io.cpp:11-27); 4 = buffer too small.
+__attribute__((visibility("default"))) int ref_tensor_text(const std::int64_t* ext, int rank,
+                                                           const char* var, std::uint64_t seed,
+                                                           const char* name, char* buf,
+                                                           std::int64_t cap) {
+  try {
+    std::vector<std::int64_t> e(ext, ext + rank);
+    std::vector<tc::Variance> v;
+    for (int i = 0; i < rank; ++i) v.push_back(var[i] == '-' ? tc::Variance::Down : tc::Variance::Up);
+    const tc::Tensor t = tc::Tensor::seeded_random(std::move(e), std::move(v), seed, name);
+    std::ostringstream os;
+    tc::write_tensor(os, t);
+    return put(os.str(), buf, cap);
+  } catch (const std::exception& e) {
+    return fail(e, buf, cap, 1);
+  }
+}
+
+// Parse TENSOR v1 text with the reference reader (src/tensor_io.cpp:53-85):
+// values into out (cap elements), *n = element count; errors as messages.
+__attribute__((visibility("default"))) int ref_read_tensor_text(const char* text, double* out,
+                                                                std::int64_t cap,
+                                                                std::int64_t* n, char* err,
+                                                                std::int64_t errcap) {
+  try {
+    std::istringstream is(text ? text : "");
+    const tc::Tensor t = tc::read_tensor(is);
+    *n = t.size();
+    if (t.size() > cap) throw std::invalid_argument("output buffer too small");
+    std::memcpy(out, t.data(), static_cast<std::size_t>(t.size()) * 8);
     return 0;
   } catch (const std::exception& e) {
     return fail(e, err, errcap, 1);

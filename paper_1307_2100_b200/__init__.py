@@ -87,6 +87,45 @@ def execute(expr: str, extents: str, seed: int = 1, positional: bool = False, wo
                  "flops": stats[3], "wall_seconds": secs.value}
 
 
+def tensor_text(extents, variance: str, seed: int, name: str = "t") -> str:
+    """TENSOR v1 text (tc::write_tensor) of Tensor::seeded_random(extents,
+    variance, seed, name)."""
+    n = int(np.prod(extents)) if len(extents) else 1
+    buf = C.create_string_buffer(64 + 32 * n + 64 * len(extents) + len(name))
+    arr = (C.c_int64 * max(1, len(extents)))(*[int(e) for e in extents])
+    rc = native.front().tcf_tensor_text(arr, len(extents), variance.encode(), seed,
+                                        name.encode(), buf, len(buf))
+    _err(rc, buf)
+    return buf.value.decode()
+
+
+def read_tensor_text(text: str) -> np.ndarray:
+    """Values of a TENSOR v1 text (tc::read_tensor), storage order."""
+    cap = max(16, text.count(" ") + text.count("\n") + 16)
+    out = np.empty(cap)
+    n = C.c_int64()
+    err = C.create_string_buffer(4096)
+    rc = native.front().tcf_read_tensor_text(text.encode(), out.ctypes.data_as(
+        C.POINTER(C.c_double)), cap, C.byref(n), err, len(err))
+    _err(rc, err)
+    return out[:n.value].copy()
+
+
+def bench_csv(experiment: str = "square3d", sizes=(100,), kernels=("GEMM",),
+              backend: str = "b200", repetitions: int = 5, seed: int = 1,
+              verify: bool = False, workers: int = 1, custom_expr: str = "",
+              custom_extents: str = ""):
+    """tc::run_bench + tc::write_bench_csv: (csv text, all sampled lines ok)."""
+    buf = C.create_string_buffer(1 << 20)
+    ok = C.c_int()
+    rc = native.front().tcf_bench_csv(
+        experiment.encode(), ",".join(str(s) for s in sizes).encode(),
+        ",".join(kernels).encode(), backend.encode(), repetitions, seed, int(verify), workers,
+        custom_expr.encode(), custom_extents.encode(), buf, len(buf), C.byref(ok))
+    _err(rc, buf)
+    return buf.value.decode(), bool(ok.value)
+
+
 def seeded(n: int, seed: int) -> np.ndarray:
     """Tensor::seeded_random's value stream (uniform [-1,1], mt19937_64)."""
     out = np.empty(int(n))

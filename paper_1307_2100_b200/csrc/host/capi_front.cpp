@@ -318,4 +318,78 @@ int tcf_release(void* handle) {
   TCF_GUARD(nullptr, 0)
 }
 
+int tcf_tensor_text(const int64_t* ext, int rank, const char* var, uint64_t seed,
+                    const char* name, char* buf, int64_t cap) {
+  try {
+    if (rank < 0 || (rank > 0 && (!ext || !var))) throw std::invalid_argument("bad tensor shape");
+    std::vector<std::int64_t> e(ext, ext + rank);
+    std::vector<tc::Variance> v;
+    for (int i = 0; i < rank; ++i) v.push_back(var[i] == '-' ? tc::Variance::Down : tc::Variance::Up);
+    const tc::Tensor t = tc::Tensor::seeded_random(std::move(e), std::move(v), seed, name ? name : "");
+    std::ostringstream os;
+    tc::write_tensor(os, t);
+    const std::string text = os.str();
+    if (static_cast<std::int64_t>(text.size()) + 1 > cap) return 4;
+    std::memcpy(buf, text.c_str(), text.size() + 1);
+    return 0;
+  }
+  TCF_GUARD(buf, cap)
+}
+
+int tcf_read_tensor_text(const char* text, double* out, int64_t cap, int64_t* n, char* err,
+                         int64_t errcap) {
+  try {
+    std::istringstream is(text ? text : "");
+    const tc::Tensor t = tc::read_tensor(is);
+    if (n) *n = t.size();
+    if (t.size() > cap) return 4;
+    std::memcpy(out, t.data(), static_cast<std::size_t>(t.size()) * 8);
+    return 0;
+  }
+  TCF_GUARD(err, errcap)
+}
+
+int tcf_bench_csv(const char* experiment, const char* sizes, const char* kernels,
+                  const char* backend, int repetitions, uint64_t seed, int verify, int workers,
+                  const char* custom_expr, const char* custom_extents, char* csv, int64_t cap,
+                  int* verified) {
+  try {
+    tc::BenchConfig cfg;
+    cfg.experiment = experiment ? experiment : "square3d";
+    {
+      std::istringstream is(sizes ? sizes : "");
+      for (std::string item; std::getline(is, item, ',');)
+        if (!item.empty()) cfg.sizes.push_back(std::stoll(item));
+    }
+    {
+      std::istringstream is(kernels ? kernels : "");
+      for (std::string item; std::getline(is, item, ',');) {
+        if (item.empty()) continue;
+        const auto k = tc::kernel_from_string(item);
+        if (!k) throw std::invalid_argument("unknown kernel '" + item + "'");
+        cfg.kernels.push_back(*k);
+      }
+    }
+    if (backend && *backend) cfg.backend = backend;
+    cfg.repetitions = repetitions;
+    cfg.seed = seed;
+    cfg.verify_sample = verify != 0;
+    cfg.workers = workers;
+    if (custom_expr) cfg.custom_expr = custom_expr;
+    cfg.custom_extents = parse_extents(custom_extents);
+    const auto rows = tc::run_bench(cfg);
+    std::ostringstream os;
+    tc::write_bench_csv(os, rows);
+    if (verified) {
+      *verified = 1;
+      for (const auto& r : rows) if (!r.verified_ok) *verified = 0;
+    }
+    const std::string text = os.str();
+    if (static_cast<std::int64_t>(text.size()) + 1 > cap) return 4;
+    std::memcpy(csv, text.c_str(), text.size() + 1);
+    return 0;
+  }
+  TCF_GUARD(csv, cap)
+}
+
 }  // extern "C"

@@ -106,6 +106,10 @@ TCF_API = {
     "tcf_device_ptrs": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "tcf_release": (i32, [vp]),
     "tcf_last_error": (cp, []),
+    "tcf_tensor_text": (i32, [P_i64, i32, cp, C.c_uint64, cp, cp, i64]),
+    "tcf_read_tensor_text": (i32, [cp, P_f64, i64, P_i64, cp, i64]),
+    "tcf_bench_csv": (i32, [cp, cp, cp, cp, i32, C.c_uint64, i32, i32, cp, cp, cp, i64,
+                            C.POINTER(C.c_int)]),
 }
 
 

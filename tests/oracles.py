@@ -61,6 +61,8 @@ def ref():
         lib.ref_seeded.argtypes = [C.c_int, P_i64, C.c_uint64, vp]
         lib.ref_gemm.argtypes = [C.c_int, C.c_int, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp,
                                  i64, cp, i64]
+        lib.ref_tensor_text.argtypes = [P_i64, C.c_int, cp, C.c_uint64, cp, cp, i64]
+        lib.ref_read_tensor_text.argtypes = [cp, vp, i64, P_i64, cp, i64]
         _cache["ref"] = lib
     return _cache["ref"]
 
@@ -167,3 +169,26 @@ def ref_report(expr: str, extents: str, positional=False):
     buf = C.create_string_buffer(1 << 20)
     rc = lib.ref_report(expr.encode(), int(positional), extents.encode(), buf, len(buf))
     return rc, buf.value.decode()
+
+
+def ref_tensor_text(ext, var: str, seed: int, name: str) -> str:
+    """TENSOR v1 text of seeded_random through the reference writer."""
+    n = int(np.prod(ext)) if len(ext) else 1
+    buf = C.create_string_buffer(64 + 32 * n + 64 * len(ext))
+    arr = (C.c_int64 * max(1, len(ext)))(*ext)
+    rc = ref().ref_tensor_text(arr, len(ext), var.encode(), seed, name.encode(), buf, len(buf))
+    assert rc == 0, buf.value
+    return buf.value.decode()
+
+
+def ref_read_tensor_text(text: str):
+    """(values, None) parsed by the reference reader, or (None, message)."""
+    cap = 1 << 22
+    out = np.empty(cap)
+    n = C.c_int64()
+    err = C.create_string_buffer(4096)
+    rc = ref().ref_read_tensor_text(text.encode(), out.ctypes.data, cap, C.byref(n), err,
+                                    len(err))
+    if rc != 0:
+        return None, err.value.decode()
+    return out[:n.value].copy(), None

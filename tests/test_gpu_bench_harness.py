@@ -1,0 +1,55 @@
+"""The reference's benchmark sweep API (tc::run_bench / tc::write_bench_csv,
+include/tc/bench.hpp:13-51) on the device backend: built-in experiments,
+forced kernels (unreachable ones as NA rows), the sampled-line verification
+(src/bench.cpp:59-112) and the CSV columns. Requires a B200."""
+import csv
+import io
+
+import pytest
+
+import paper_1307_2100_b200 as T
+
+pytestmark = pytest.mark.gpu
+COLS = ["experiment", "expression", "size", "kernel", "backend", "repetitions",
+        "median_seconds", "gflops", "packed_bytes"]
+
+
+def rows(text):
+    r = list(csv.reader(io.StringIO(text)))
+    assert r[0] == COLS
+    return [dict(zip(COLS, x)) for x in r[1:]]
+
+
+def test_square3d_rows_verify_and_report(dev):
+    text, ok = T.bench_csv("square3d", sizes=(64, 96), kernels=("GEMM", "COPY+GEMM", "GEMV", "DOT"),
+                           repetitions=3, seed=3, verify=True)
+    assert ok
+    rs = rows(text)
+    assert len(rs) == 2 * 2 * 4  # sizes x expressions x kernels
+    assert {r["expression"] for r in rs} == {"R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]",
+                                             "R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]"}
+    for r in rs:
+        assert r["backend"] == "b200" and r["repetitions"] == "3"
+        if r["median_seconds"] != "NA":
+            assert float(r["gflops"]) > 0 and float(r["median_seconds"]) > 0
+
+
+def test_gr4d_and_cc4d_with_sampled_verification(dev):
+    for exp in ("gr4d", "cc4d"):
+        text, ok = T.bench_csv(exp, sizes=(24,), kernels=("GEMM", "COPY+GEMM", "GER", "DOT"),
+                               repetitions=2, seed=5, verify=True)
+        assert ok, exp
+        assert len(rows(text)) == 2 * 4
+
+
+def test_custom_experiment_and_errors(dev):
+    text, ok = T.bench_csv("custom", sizes=(1,), kernels=("GEMM",), repetitions=2, verify=True,
+                           custom_expr="C[+i,+j] = A[+i,+k] * B[-k,+j]",
+                           custom_extents="i=130,j=70,k=50")
+    assert ok and rows(text)[0]["expression"] == "C[+i,+j] = A[+i,+k] * B[-k,+j]"
+    with pytest.raises(ValueError, match="unknown experiment"):
+        T.bench_csv("nope", sizes=(4,))
+    with pytest.raises(ValueError, match="repetitions must be >= 1"):
+        T.bench_csv("square3d", sizes=(4,), repetitions=0)
+    with pytest.raises(ValueError, match="size sweep must be nonempty"):
+        T.bench_csv("square3d", sizes=())
