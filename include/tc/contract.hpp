@@ -379,8 +379,11 @@ struct DeviceRecipe {
 
 /// Lower a validated contraction to one device recipe. `index_groups` allows
 /// the L4 form (operands read in place through composite tensor-map boxes)
-/// where L3 would otherwise permute an operand.
-DeviceRecipe lower(const ValidatedContraction& v, bool index_groups = true);
+/// where L3 would otherwise permute an operand. `layout`, when given, is the
+/// contraction whose storage the operands and output live in (v a slab of it:
+/// same labels, smaller extents): strides come from it, extents from v.
+DeviceRecipe lower(const ValidatedContraction& v, bool index_groups = true,
+                   const ValidatedContraction* layout = nullptr);
 
 /// A contraction lowered once and bound to device buffers, for repeated
 /// execution without host round trips (no reference counterpart; bench.py
@@ -412,8 +415,10 @@ class PreparedContraction {
   /// copy stream as they complete. Needs page-locked host buffers for the
   /// copies to overlap; otherwise (or when no such label exists) it is
   /// upload + run + download. `slabs` <= 0 picks ~16 MB slabs (up to 64;
-  /// below 32 MB of streamed data the plain path is used). Returns the slab
-  /// count.
+  /// below 32 MB of streamed data the plain path is used). When the output
+  /// is smaller than the operand that would have to go up whole, slabs of a
+  /// contracted label are streamed instead (both operands by 2-D copies, C
+  /// accumulated on the device, downloaded once). Returns the slab count.
   int run_streamed(const double* left, const double* right, double* out, int slabs = 0);
 
   const DeviceRecipe& recipe() const { return recipe_; }
@@ -431,6 +436,9 @@ class PreparedContraction {
   ValidatedContraction v_;
   bool groups_ok_ = true;  // L4 allowed (cleared if the device refuses it)
   int auto_slabs_ = -1;    // run_streamed's automatic slab count, once decided
+  int stream_mode_ = -1;   // run_streamed: 0 output-label slabs, 1 + label: contracted slabs
+  int run_streamed_k(const double* left, const double* right, double* out, int slabs,
+                     int label);
   int device_ = 0;
   std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
   double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;

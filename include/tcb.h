@@ -69,6 +69,12 @@ int tcb_stream_sync(void* stream);
 void* tcb_current_stream(void);
 /* Asynchronous copy in any direction on `stream` (NULL: current stream). */
 int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* Asynchronous strided copy: `height` rows of `width` bytes, row r from
+ * src + r*spitch to dst + r*dpitch (pitches in bytes; NULL stream: current).
+ * Moves a slab of a middle mode of a column-major tensor in one call (the
+ * 2-D H2D of SURVEY §8e; cudaMemcpy2DAsync underneath). */
+int tcb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                       int64_t width, int64_t height, void* stream);
 /* *pinned = 1 when `ptr` is page-locked host memory (registered or allocated). */
 int tcb_host_is_pinned(const void* ptr, int* pinned);
 

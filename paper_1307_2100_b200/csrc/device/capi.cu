@@ -260,6 +260,23 @@ int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
   return TCB_OK;
 }
 
+int tcb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                       int64_t width, int64_t height, void* stream) {
+  TCB_TRY_INIT();
+  if (width < 0 || height < 0 || dpitch < width || spitch < width)
+    return set_error(TCB_EINVAL, "copy2d: negative size or pitch below width");
+  if (width == 0 || height == 0) return TCB_OK;
+  if (height == 1) {
+    TCB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(width), cudaMemcpyDefault,
+                             stream_or_current(stream)));
+    return TCB_OK;
+  }
+  TCB_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(dpitch), src, static_cast<size_t>(spitch),
+                             static_cast<size_t>(width), static_cast<size_t>(height),
+                             cudaMemcpyDefault, stream_or_current(stream)));
+  return TCB_OK;
+}
+
 int tcb_host_is_pinned(const void* ptr, int* pinned) {
   TCB_TRY_INIT();
   if (!pinned) return set_error(TCB_EINVAL, "tcb_host_is_pinned: null pointer");

@@ -4,6 +4,7 @@
 // call per slice (src/executor.cpp:287-369, run_range :102-283). Here the
 // contraction is lowered once (lower.cpp) and executed as permutations + one
 // device launch through the C-ABI (tcb.h). Host C++ only: no CUDA headers.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -208,16 +209,54 @@ tcb_gemm_desc desc_of(const DeviceRecipe& r) {
 namespace {
 // L4 recipes the device cannot map (the host rules mirror the device's, so
 // this is a safety net) are lowered again without index groups.
-DeviceRecipe lower_checked(const ValidatedContraction& v, bool* groups_ok) {
-  DeviceRecipe r = lower(v, *groups_ok);
+DeviceRecipe lower_checked(const ValidatedContraction& v, bool* groups_ok,
+                           const ValidatedContraction* layout = nullptr) {
+  DeviceRecipe r = lower(v, *groups_ok, layout);
   if (r.layout == "L4") {
     const tcb_gemm_desc d = desc_of(r);
     if (tcb_gemm_check(&d) != TCB_OK) {
       *groups_ok = false;
-      r = lower(v, false);
+      r = lower(v, false, layout);
     }
   }
   return r;
+}
+
+// A contracted label whose slabs the streamed path can upload with one 2-D
+// copy per operand and contract in place: the last mode of its contracted
+// run in both operands (so slicing it keeps every flattened index group
+// chained), extent >= 2, room for two slabs with rows of at least 4 KB.
+// -1 if none; the widest rows win.
+int k_stream_label(const ValidatedContraction& v) {
+  int best = -1;
+  std::int64_t best_rows = 0;
+  for (int id : v.contracted) {
+    const LabelInfo& li = v.labels[static_cast<std::size_t>(id)];
+    if (li.extent < 2) continue;
+    bool ok = true;
+    std::int64_t row_min = std::numeric_limits<std::int64_t>::max();
+    for (int side = 0; side < 2 && ok; ++side) {
+      const int mode = side ? li.right_mode : li.left_mode;
+      const int rank = side ? v.right_rank() : v.left_rank();
+      std::int64_t below = 1;
+      for (int m = 0; m < mode; ++m)
+        below *= (side ? v.label_at_right_mode(m) : v.label_at_left_mode(m)).extent;
+      // the next non-unit mode must not be contracted (end of the run)
+      for (int m = mode + 1; m < rank; ++m) {
+        const LabelInfo& nx = side ? v.label_at_right_mode(m) : v.label_at_left_mode(m);
+        if (nx.extent == 1) continue;
+        ok = !nx.contracted;
+        break;
+      }
+      row_min = std::min(row_min, below * 8);
+    }
+    if (!ok || row_min * li.extent < 2 * 4096) continue;
+    if (best < 0 || row_min > best_rows) {
+      best = id;
+      best_rows = row_min;
+    }
+  }
+  return best;
 }
 }  // namespace
 
@@ -340,6 +379,28 @@ struct PreparedContraction::Pipes {
 int PreparedContraction::run_streamed(const double* left, const double* right, double* out,
                                       int slabs) {
   check(tcb_init(device_), "tcb_init");
+  // Two ways to stream (chosen once): slabs of the output's outermost label
+  // (below: the other operand is uploaded whole first, output slabs go down
+  // as they complete) or slabs of a contracted label (run_streamed_k: both
+  // operands stream, C accumulates on the device and goes down at the end).
+  // The one that leaves fewer bytes outside the overlap wins.
+  if (stream_mode_ < 0) {
+    stream_mode_ = 0;
+    const int kl = recipe_.permutes.empty() ? k_stream_label(v_) : -1;
+    if (kl >= 0) {
+      std::int64_t other = nl_ + nr_;  // unoverlapped bytes of the output-label mode
+      const auto& outs = v_.spec.output.indices;
+      if (!outs.empty()) {
+        const LabelInfo& li = v_.labels[static_cast<std::size_t>(v_.label_index(outs.back().label))];
+        const bool l = li.left_mode >= 0;
+        if ((l ? li.left_mode == v_.left_rank() - 1 : li.right_mode == v_.right_rank() - 1) &&
+            li.extent >= 2)
+          other = l ? nr_ : nl_;
+      }
+      if (no_ < other) stream_mode_ = 1 + kl;
+    }
+  }
+  if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1);
   // the stream label: outermost output label, outermost mode of its operand
   const auto& outs = v_.spec.output.indices;
   int label = outs.empty() ? -1 : v_.label_index(outs.back().label);
@@ -499,6 +560,96 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     e0 += e;
   }
   check(tcb_stream_sync(down), "sync");
+  launches_ = tcb_launch_count() - before;
+  return slabs;
+}
+
+// Streamed evaluation over slabs of contracted label `label`: slab s of each
+// operand (one 2-D copy: rows of stride*e elements at pitch stride*E) goes up
+// on the copy stream while slab s-1 is contracted; the slab GEMMs accumulate
+// into C on the device (beta = 1 after the first) and C goes down once.
+int PreparedContraction::run_streamed_k(const double* left, const double* right, double* out,
+                                        int slabs, int label) {
+  const LabelInfo& kl = v_.labels[static_cast<std::size_t>(label)];
+  const std::int64_t E = kl.extent;
+  if (slabs <= 0)  // ~4 MB of operand data per slab, 2..64 slabs
+    slabs = static_cast<int>(std::clamp<std::int64_t>((nl_ + nr_) * 8 / (4LL << 20), 2, 64));
+  slabs = static_cast<int>(std::min<std::int64_t>(slabs, E));
+  int pinned_l = 0, pinned_r = 0, pinned_o = 0;
+  tcb_host_is_pinned(left, &pinned_l);
+  tcb_host_is_pinned(right, &pinned_r);
+  tcb_host_is_pinned(out, &pinned_o);
+  // (stride of the label, rows above it) per operand, in elements
+  auto geom = [&](bool right_side) {
+    const int mode = right_side ? kl.right_mode : kl.left_mode;
+    const int rank = right_side ? v_.right_rank() : v_.left_rank();
+    std::int64_t below = 1, above = 1;
+    for (int m = 0; m < rank; ++m) {
+      const std::int64_t e = (right_side ? v_.label_at_right_mode(m) : v_.label_at_left_mode(m)).extent;
+      if (m < mode) below *= e;
+      if (m > mode) above *= e;
+    }
+    return std::make_pair(below, above);
+  };
+  const auto [sa, ha] = geom(false);
+  const auto [sb, hb] = geom(true);
+  // copy rows of at least 4 KB per slab
+  slabs = static_cast<int>(std::min<std::int64_t>(slabs, std::min(sa, sb) * 8 * E / 4096));
+  if (slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
+    upload(left, right);
+    run();
+    download(out);
+    return 1;
+  }
+  std::map<std::int64_t, DeviceRecipe> recipes;  // one per distinct slab extent
+  std::vector<std::int64_t> sizes;
+  for (int i = 0; i < slabs; ++i) {
+    const std::int64_t e = E / slabs + (i < E % slabs ? 1 : 0);
+    sizes.push_back(e);
+    if (recipes.count(e)) continue;
+    ValidatedContraction sv = v_;
+    sv.labels[static_cast<std::size_t>(label)].extent = e;
+    bool ok = groups_ok_;
+    DeviceRecipe r = lower_checked(sv, &ok, &v_);
+    if (!r.permutes.empty()) {  // not expected (the full recipe permutes nothing)
+      upload(left, right);
+      run();
+      download(out);
+      return 1;
+    }
+    recipes.emplace(e, std::move(r));
+  }
+  if (!pipes_) {
+    pipes_ = std::make_unique<Pipes>();
+    check(tcb_stream_create(&pipes_->up), "stream");
+    check(tcb_stream_create(&pipes_->down), "stream");
+  }
+  Pipes& h = *pipes_;
+  h.next = 0;
+  void* compute = tcb_current_stream();
+  const std::int64_t before = tcb_launch_count();
+  std::int64_t e0 = 0;
+  for (int s = 0; s < slabs; ++s) {
+    const std::int64_t e = sizes[static_cast<std::size_t>(s)];
+    check(tcb_memcpy2d_async(dl_ + e0 * sa, sa * E * 8, left + e0 * sa, sa * E * 8, sa * e * 8,
+                             ha, h.up),
+          "upload");
+    check(tcb_memcpy2d_async(dr_ + e0 * sb, sb * E * 8, right + e0 * sb, sb * E * 8, sb * e * 8,
+                             hb, h.up),
+          "upload");
+    void* ready = h.event();
+    check(tcb_event_record(ready, h.up), "event");
+    check(tcb_stream_wait_event(compute, ready), "event");
+    tcb_gemm_desc d = desc_of(recipes.at(e));
+    d.beta = s == 0 ? 0.0 : 1.0;
+    check(tcb_gemm(&d, dl_ + e0 * sa, dr_ + e0 * sb, do_), "contraction");
+    e0 += e;
+  }
+  void* done = h.event();
+  check(tcb_event_record(done, compute), "event");
+  check(tcb_stream_wait_event(h.down, done), "event");
+  check(tcb_memcpy_async(out, do_, no_ * 8, h.down), "download");
+  check(tcb_stream_sync(h.down), "sync");
   launches_ = tcb_launch_count() - before;
   return slabs;
 }

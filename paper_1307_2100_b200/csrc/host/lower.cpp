@@ -40,19 +40,23 @@ struct Side {
   std::int64_t elements = 1;
 };
 
-Side side_of(const ValidatedContraction& v, bool right) {
+// Strides come from `layout` (the storage the operand lives in: the full
+// contraction when v is a slab of it), iteration extents from v.
+Side side_of(const ValidatedContraction& v, const ValidatedContraction& layout, bool right) {
   Side s;
   s.stride.assign(v.labels.size(), 0);
   const int rank = right ? v.right_rank() : v.left_rank();
-  std::int64_t run = 1;
+  std::int64_t run = 1, elems = 1;
   for (int m = 0; m < rank; ++m) {
     const LabelInfo& li = right ? v.label_at_right_mode(m) : v.label_at_left_mode(m);
+    const LabelInfo& lo = right ? layout.label_at_right_mode(m) : layout.label_at_left_mode(m);
     const int id = v.label_index(li.label);
     s.stride[static_cast<std::size_t>(id)] = run;
-    run *= li.extent;
+    run *= lo.extent;
+    elems *= li.extent;
     if (li.extent > 1) s.modes.push_back(id);
   }
-  s.elements = run;
+  s.elements = elems;
   return s;
 }
 
@@ -253,19 +257,21 @@ std::string DeviceRecipe::summary() const {
   return os.str();
 }
 
-DeviceRecipe lower(const ValidatedContraction& v, bool index_groups) {
+DeviceRecipe lower(const ValidatedContraction& v, bool index_groups,
+                   const ValidatedContraction* layout) {
   // TC_INDEX_GROUPS=0 disables L4 (A/B comparisons against L3)
   if (const char* env = std::getenv("TC_INDEX_GROUPS"); env != nullptr && env[0] == '0')
     index_groups = false;
+  const ValidatedContraction& lay = layout ? *layout : v;
   const std::size_t nlab = v.labels.size();
-  Side A = side_of(v, false), B = side_of(v, true);
+  Side A = side_of(v, lay, false), B = side_of(v, lay, true);
   std::vector<std::int64_t> ostr(nlab, 0);
   {
     std::int64_t run = 1;
     for (const auto& ix : v.spec.output.indices) {
       const int id = v.label_index(ix.label);
       ostr[static_cast<std::size_t>(id)] = run;
-      run *= v.labels[static_cast<std::size_t>(id)].extent;
+      run *= lay.labels[static_cast<std::size_t>(id)].extent;
     }
   }
   auto is_k = [&](int id) { return v.labels[static_cast<std::size_t>(id)].contracted; };

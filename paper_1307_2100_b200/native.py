@@ -70,6 +70,7 @@ TCB_API = {
     "tcb_stream_sync": (i32, [vp]),
     "tcb_current_stream": (vp, []),
     "tcb_memcpy_async": (i32, [vp, vp, i64, vp]),
+    "tcb_memcpy2d_async": (i32, [vp, i64, vp, i64, i64, i64, vp]),
     "tcb_host_is_pinned": (i32, [vp, C.POINTER(C.c_int)]),
     "tcb_gemm": (i32, [C.POINTER(GemmDesc), vp, vp, vp]),
     "tcb_gemm_check": (i32, [C.POINTER(GemmDesc)]),
