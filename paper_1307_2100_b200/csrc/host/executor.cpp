@@ -225,8 +225,12 @@ DeviceRecipe lower_checked(const ValidatedContraction& v, bool* groups_ok,
 // A contracted label whose slabs the streamed path can upload with one 2-D
 // copy per operand and contract in place: the last mode of its contracted
 // run in both operands (so slicing it keeps every flattened index group
-// chained), extent >= 2, room for two slabs with rows of at least 4 KB.
+// chained), extent >= 2, room for two slabs with copy rows of at least 32 KB
+// (narrower 2-D rows slow the DMA below the 1-D rate: cfg1's 4 KB rows lost
+// to the output-label mode).
 // -1 if none; the widest rows win.
+constexpr std::int64_t kMinRow = 32 << 10;
+
 int k_stream_label(const ValidatedContraction& v) {
   int best = -1;
   std::int64_t best_rows = 0;
@@ -250,7 +254,7 @@ int k_stream_label(const ValidatedContraction& v) {
       }
       row_min = std::min(row_min, below * 8);
     }
-    if (!ok || row_min * li.extent < 2 * 4096) continue;
+    if (!ok || row_min * li.extent < 2 * kMinRow) continue;
     if (best < 0 || row_min > best_rows) {
       best = id;
       best_rows = row_min;
@@ -593,8 +597,8 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   };
   const auto [sa, ha] = geom(false);
   const auto [sb, hb] = geom(true);
-  // copy rows of at least 4 KB per slab
-  slabs = static_cast<int>(std::min<std::int64_t>(slabs, std::min(sa, sb) * 8 * E / 4096));
+  // copy rows of at least 32 KB per slab
+  slabs = static_cast<int>(std::min<std::int64_t>(slabs, std::min(sa, sb) * 8 * E / kMinRow));
   if (slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
     upload(left, right);
     run();

@@ -185,8 +185,8 @@ def test_cfg5_full_size_sampled(dev):
     ("left-streamed", "R[+b,+a] = B[+k,+b] * A[-k,+a]", "a=50,b=30,k=20"),
     # output smaller than the operand that would go up whole: slabs of the
     # contracted label l (2-D copies, C accumulated on the device)
-    ("k-streamed", "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=96,j=40,k=64,l=40"),
-    ("k-streamed-L4", "C[+a,+b,+c] = A[+a,+k,+c,+l] * B[-k,+b,-l]", "a=32,b=24,c=5,k=16,l=20"),
+    ("k-streamed", "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=96,j=40,k=512,l=40"),
+    ("k-streamed-L4", "C[+a,+b,+c] = A[+a,+k,+c,+l] * B[-k,+b,-l]", "a=32,b=256,c=5,k=16,l=40"),
 ])
 def test_streamed_host_path_matches(dev, name, e, x):
     # tc::PreparedContraction::run_streamed: slabs of the operand carrying the
