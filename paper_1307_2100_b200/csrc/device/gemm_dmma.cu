@@ -623,6 +623,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         trace_mark(p, 10 + 3 * (static_cast<int>(tcount) - 1), tl);
       if (gcons == 0) trace_mark(p, 1, tl);
       if (gcons == 8) trace_mark(p, 7, tl);
+      if (tcount == 2 && kb == kb0 + 4) trace_mark(p, 30, tl);
+      if (tcount == 2 && kb == kb0 + 8) trace_mark(p, 31, tl);
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {

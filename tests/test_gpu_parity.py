@@ -212,3 +212,26 @@ def test_streamed_host_path_matches(dev, name, e, x):
         O.max_rel_error(out, ref) <= TOL
     for a in (L, R, out):
         dev.tcb_host_unregister(a.ctypes.data)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_full_size_scaling_is_exact_and_additive(dev, cfg):
+    """Size-independent properties at the BASELINE sizes: scaling an operand
+    by a power of two scales C exactly (every product and partial sum scales
+    exactly, so the same summation order gives the same bits x 4), and C is
+    additive in an operand to within rounding."""
+    import bench
+    e, x, _ = bench.CONFIGS[cfg]
+    p = T.Prepared(e, x)
+    inf = p.info()
+    L = T.seeded(inf["left"], 1)
+    R = T.seeded(inf["right"], 2)
+    R2 = T.seeded(inf["right"], 3)
+    c1, c4, c2, c12 = (np.empty(inf["output"]) for _ in range(4))
+    for (a, b), out in (((L, R), c1), ((L, 4.0 * R), c4), ((L, R2), c2), ((L, R + R2), c12)):
+        p.upload(a, b)
+        p.run()
+        p.download(out)
+    assert np.array_equal((4.0 * c1).view(np.uint64), c4.view(np.uint64)), cfg
+    assert O.rel_frobenius(c12, c1 + c2) <= TOL, cfg
+    p.close()

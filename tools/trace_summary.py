@@ -22,6 +22,12 @@ for line in open(sys.argv[1]):
             loop = [(x[nxt] - x[c]) / 1e3 for x in t if x[c] and x[nxt]]
             print(f"  tile {j + 1}: epilogue {med(epi):6.2f}  wait first data {med(gap):6.2f}  "
                   f"mainloop {med(loop):7.2f} us (median over CTAs)")
+    if w == 32:  # slots 30/31: tile 2 after 4 / 8 k-blocks (ramp inside a tile)
+        r = [((x[30] - x[13]) / 4e3, (x[31] - x[30]) / 4e3, (x[14] - x[31]) / 8e3)
+             for x in t if x[13] and x[30] and x[31] and x[14]]
+        if r:
+            print("  tile 2 us per k-block: blocks 0-3 %.3f, 4-7 %.3f, 8-end %.3f" %
+                  tuple(statistics.median(v[i] for v in r) for i in range(3)))
     starts = [x[0] - t0 for x in t]
     print(f"  CTA start skew: median {statistics.median(starts)/1e3:.2f} max {max(starts)/1e3:.2f} us")
     r1 = [(x[7] - x[1]) / 8e3 for x in t if x[7] and x[1]]
