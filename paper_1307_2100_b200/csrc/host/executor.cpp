@@ -6,6 +6,7 @@
 // device launch through the C-ABI (tcb.h). Host C++ only: no CUDA headers.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -230,6 +231,14 @@ DeviceRecipe lower_checked(const ValidatedContraction& v, bool* groups_ok,
 // to the output-label mode).
 // -1 if none; the widest rows win.
 constexpr std::int64_t kMinRow = 32 << 10;
+// output-label mode: streamed operand + output bytes per slab (TC_SLAB_MB overrides)
+std::int64_t slab_bytes() {
+  static const std::int64_t b = [] {
+    const char* e = std::getenv("TC_SLAB_MB");
+    return (e ? std::max(1LL, std::atoll(e)) : 16LL) << 20;
+  }();
+  return b;
+}
 
 int k_stream_label(const ValidatedContraction& v) {
   int best = -1;
@@ -425,13 +434,14 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
         label = -1;
   }
   if (label >= 0 && slabs <= 0) {
-    // auto (decided once per prepared contraction): ~16 MB of streamed operand
-    // + output per slab, up to 64 slabs, but no thinner than keeps both slab
+    // auto (decided once per prepared contraction): ~16 MB per slab in the
+    // busier copy direction, up to 64 slabs, but no thinner than keeps both slab
     // sizes' GEMM tiles (128x128) as full as the whole contraction's — cfg4's
     // 64 one-j slabs would leave every tile half empty
     if (auto_slabs_ < 0) {
-      const std::int64_t bytes = ((on_left ? nl_ : nr_) + no_) * 8;
-      int want = static_cast<int>(std::min<std::int64_t>(64, bytes / (16LL << 20)));
+      // the busier copy direction sets the slab size (16 MB of it per slab)
+      const std::int64_t bytes = std::max(on_left ? nl_ : nr_, no_) * 8;
+      int want = static_cast<int>(std::min<std::int64_t>(64, bytes / slab_bytes()));
       const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
       auto tile_eff = [&](std::int64_t e) {
         ValidatedContraction sv = v_;
