@@ -117,6 +117,7 @@ int tcb_set_stream(void* stream) {
   TCB_TRY_INIT();
   ThreadState& st = state();
   st.stream = stream ? static_cast<cudaStream_t>(stream) : st.own_stream;
+  st.pdl_ok = false;
   return TCB_OK;
 }
 
@@ -145,6 +146,7 @@ int tcb_free(void* dptr) {
 int tcb_memset0(void* dptr, int64_t bytes) {
   TCB_TRY_INIT();
   if (bytes <= 0) return TCB_OK;
+  note_stream_op();
   TCB_CUDA(cudaMemsetAsync(dptr, 0, static_cast<size_t>(bytes), state().stream));
   return TCB_OK;
 }
@@ -153,6 +155,7 @@ static int copy(void* dst, const void* src, int64_t bytes, cudaMemcpyKind kind) 
   TCB_TRY_INIT();
   if (bytes < 0) return set_error(TCB_EINVAL, "copy: negative size");
   if (bytes == 0) return TCB_OK;
+  note_stream_op();
   TCB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), kind, state().stream));
   if (kind == cudaMemcpyDeviceToHost) TCB_CUDA(cudaStreamSynchronize(state().stream));
   return TCB_OK;
@@ -236,6 +239,7 @@ int tcb_event_record(void* event, void* stream) {
 
 int tcb_stream_wait_event(void* stream, void* event) {
   TCB_TRY_INIT();
+  note_stream_op(stream_or_current(stream));
   TCB_CUDA(cudaStreamWaitEvent(stream_or_current(stream), static_cast<cudaEvent_t>(event), 0));
   return TCB_OK;
 }
@@ -255,6 +259,7 @@ int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
   TCB_TRY_INIT();
   if (bytes < 0) return set_error(TCB_EINVAL, "copy: negative size");
   if (bytes == 0) return TCB_OK;
+  note_stream_op(stream_or_current(stream));
   TCB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
                            stream_or_current(stream)));
   return TCB_OK;
@@ -266,6 +271,7 @@ int tcb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitc
   if (width < 0 || height < 0 || dpitch < width || spitch < width)
     return set_error(TCB_EINVAL, "copy2d: negative size or pitch below width");
   if (width == 0 || height == 0) return TCB_OK;
+  note_stream_op(stream_or_current(stream));
   if (height == 1) {
     TCB_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(width), cudaMemcpyDefault,
                              stream_or_current(stream)));
@@ -487,6 +493,7 @@ int tcb_ddot(int64_t k, const double* x, int64_t incx, const double* y, int64_t 
   d.beta = 0.0;
   int rc = tcb_gemm(&d, x, y, dres);
   if (rc == TCB_OK) {
+    note_stream_op();
     cudaError_t e = cudaMemcpyAsync(result_host, dres, 8, cudaMemcpyDeviceToHost, st.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st.stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "dot result copy");

@@ -161,6 +161,13 @@ __device__ __forceinline__ void tma_store5(const CUtensorMap* map, uint32_t src,
       : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// Programmatic dependent launch: let the next grid in the stream start (its
+// CTAs are scheduled as ours exit), and wait for the previous grid to have
+// completed before this thread's first global write.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // the bulk stores have finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -475,6 +482,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
   __syncthreads();
+  pdl_launch_dependents();
 
   if (tid < PTHREADS) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
@@ -501,6 +509,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             c[d] = static_cast<int>(prog_coord(p.pc, d, v));
           }
           mbar_wait(stg_full, t & 1);
+          pdl_wait();
           tma_store5(&tmC, stg, c[0], c[1], c[2], c[3], c[4]);
           bulk_wait_read();  // staging may be overwritten once read
           mbar_arrive(stg_empty);
@@ -526,6 +535,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         asm volatile("bar.sync 2, 96;" ::: "memory");
         mbar_wait(stg_full, t & 1);
+        pdl_wait();
         double* Cb = p.C + oc;
         // warp w writes columns n = w, w+3, ...; lanes walk m (coalesced in C).
         // alpha was applied by the consumers; plain copies keep the FP64 pipe
@@ -714,6 +724,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // 3) split s reduces pairs [s*P/S, (s+1)*P/S) of the tile, summing the S
       //    partials in split order — bit-reproducible, spread over all S CTAs.
       const int64_t tile = u / p.splits;
+      pdl_wait();  // the previous grid may still read the workspace / counters
       double2* base = reinterpret_cast<double2*>(p.ws) + tile * p.splits * (BM * BN / 2);
       double2* part = base + un.split * (BM * BN / 2);
 #pragma unroll
@@ -798,6 +809,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 
     consumer_sync();
+    pdl_wait();
     // Branch-free stores (predicated STG): one unrolled copy per beta mode so
     // the epilogue stays small (it runs once per tile, off the I-cache-hot loop).
     int64_t coff[4][2];
@@ -1107,7 +1119,7 @@ bool kmajor_of(const Group& outer, const Group& kg) {
 
 template <bool AK, bool BK_, bool TMA>
 cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap& tb,
-                       const CUtensorMap& tc, int grid, cudaStream_t s) {
+                       const CUtensorMap& tc, int grid, cudaStream_t s, bool pdl) {
   const bool split = p.splits > 1;
   auto kern = split ? dgemm_dmma_kernel<AK, BK_, TMA, true> : dgemm_dmma_kernel<AK, BK_, TMA, false>;
   const int smem = split ? smem_bytes<false>() : smem_bytes<TMA>();
@@ -1127,15 +1139,48 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
   cfg.blockDim = dim3(NTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // split-K CTAs wait on each other
   attr[0].val.cooperative = p.splits > 1 ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p, ta, tb, tc);
+  cfg.numAttrs = pdl ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, ta, tb, tc);
+  if (e != cudaSuccess && pdl) {  // combination refused: plain stream order
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p, ta, tb, tc);
+  }
+  return e;
 }
 
 }  // namespace
+
+// Byte ranges [lo, hi) an operand / the output of a descriptor can touch
+// (strides are positive; batch offsets included).
+std::pair<uintptr_t, uintptr_t> operand_range(const tcb_gemm_desc& d, const double* X, bool left) {
+  int64_t last = 0;
+  if (has_groups(d)) {
+    const int g = left ? d.g_m : d.g_n;
+    for (int i = 0; i < g; ++i)
+      last += (left ? d.m_ext[i] - 1 : d.n_ext[i] - 1) * (left ? d.a_m_str[i] : d.b_n_str[i]);
+    for (int i = 0; i < d.g_k; ++i) last += (d.k_ext[i] - 1) * (left ? d.a_k_str[i] : d.b_k_str[i]);
+  } else {
+    last += left ? (d.m - 1) * d.a_sm + (d.k - 1) * d.a_sk : (d.k - 1) * d.b_sk + (d.n - 1) * d.b_sn;
+  }
+  for (int i = 0; i < d.nbatch; ++i) last += (d.bat_ext[i] - 1) * (left ? d.bat_sa[i] : d.bat_sb[i]);
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(X);
+  return {lo, lo + static_cast<uintptr_t>(last + 1) * 8};
+}
+std::pair<uintptr_t, uintptr_t> output_range(const tcb_gemm_desc& d, const double* C) {
+  int64_t last = 0;
+  for (int i = 0; i < d.c_nrow; ++i) last += (d.c_row_ext[i] - 1) * d.c_row_str[i];
+  for (int i = 0; i < d.c_ncol; ++i) last += (d.c_col_ext[i] - 1) * d.c_col_str[i];
+  for (int i = 0; i < d.nbatch; ++i) last += (d.bat_ext[i] - 1) * d.bat_sc[i];
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(C);
+  return {lo, lo + static_cast<uintptr_t>(last + 1) * 8};
+}
 
 int launch_scale(const tcb_gemm_desc& d, double* C) {
   Params p{};
@@ -1248,6 +1293,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     }
     if (st.last_splits != splits || st.last_tiles != tiles ||
         static_cast<int64_t>(st.epoch + 2) * splits >= (1LL << 31)) {
+      note_stream_op();
       TCB_CUDA(cudaMemsetAsync(st.counters, 0, st.counters_n * sizeof(unsigned), st.stream));
       st.epoch = 0;
     }
@@ -1278,6 +1324,15 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
 
   const int grid = static_cast<int>(std::min<int64_t>(p.units, sms));
+  // Programmatic dependent launch when the previous operation on our own
+  // stream was a GEMM whose output does not overlap this one's operands
+  // (read before griddepcontrol.wait). TCB_NO_PDL=1 disables it.
+  static const bool no_pdl = getenv("TCB_NO_PDL") != nullptr;
+  const auto [alo, ahi] = operand_range(d, A, true);
+  const auto [blo, bhi] = operand_range(d, B, false);
+  const bool pdl = !no_pdl && st.pdl_ok && st.stream == st.own_stream &&
+                   (ahi <= st.pdl_lo || alo >= st.pdl_hi) &&
+                   (bhi <= st.pdl_lo || blo >= st.pdl_hi);
   // TCB_TRACE=<file>: append per-CTA phase timestamps of this launch (diagnostics)
   static const char* trace_path = getenv("TCB_TRACE");
   unsigned long long* trace = nullptr;
@@ -1286,26 +1341,34 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     TCB_CUDA(cudaMemsetAsync(trace, 0, grid * 32 * sizeof(unsigned long long), st.stream));
   }
   p.trace = trace;
+  if (trace) note_stream_op();
   static const int diag = getenv("TCB_DIAG") ? atoi(getenv("TCB_DIAG")) : 0;
   p.diag = diag;
   cudaError_t e;
   if (tma) {
-    if (a_k && b_k) e = launch_one<true, true, true>(p, ta, tb, tc, grid, st.stream);
-    else if (a_k) e = launch_one<true, false, true>(p, ta, tb, tc, grid, st.stream);
-    else if (b_k) e = launch_one<false, true, true>(p, ta, tb, tc, grid, st.stream);
-    else e = launch_one<false, false, true>(p, ta, tb, tc, grid, st.stream);
+    if (a_k && b_k) e = launch_one<true, true, true>(p, ta, tb, tc, grid, st.stream, pdl);
+    else if (a_k) e = launch_one<true, false, true>(p, ta, tb, tc, grid, st.stream, pdl);
+    else if (b_k) e = launch_one<false, true, true>(p, ta, tb, tc, grid, st.stream, pdl);
+    else e = launch_one<false, false, true>(p, ta, tb, tc, grid, st.stream, pdl);
   } else {
-    if (a_k && b_k) e = launch_one<true, true, false>(p, ta, tb, tc, grid, st.stream);
-    else if (a_k) e = launch_one<true, false, false>(p, ta, tb, tc, grid, st.stream);
-    else if (b_k) e = launch_one<false, true, false>(p, ta, tb, tc, grid, st.stream);
-    else e = launch_one<false, false, false>(p, ta, tb, tc, grid, st.stream);
+    if (a_k && b_k) e = launch_one<true, true, false>(p, ta, tb, tc, grid, st.stream, pdl);
+    else if (a_k) e = launch_one<true, false, false>(p, ta, tb, tc, grid, st.stream, pdl);
+    else if (b_k) e = launch_one<false, true, false>(p, ta, tb, tc, grid, st.stream, pdl);
+    else e = launch_one<false, false, false>(p, ta, tb, tc, grid, st.stream, pdl);
   }
   if (e != cudaSuccess) {
     st.last_splits = 0;
     return cuda_fail(e, "dgemm_dmma launch");
   }
   ++st.launches;
+  {
+    const auto [clo, chi] = output_range(d, C);
+    st.pdl_ok = true;
+    st.pdl_lo = clo;
+    st.pdl_hi = chi;
+  }
   if (trace) {
+    note_stream_op();
     std::vector<unsigned long long> h(static_cast<size_t>(grid) * 32);
     TCB_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st.stream));
     TCB_CUDA(cudaStreamSynchronize(st.stream));

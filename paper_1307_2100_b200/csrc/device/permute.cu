@@ -160,6 +160,7 @@ int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const d
   if (total == 0) return TCB_OK;
   ThreadState& st = state();
   if (e.empty()) {  // a single element
+    note_stream_op();
     TCB_CUDA(cudaMemcpyAsync(dst, src, 8, cudaMemcpyDeviceToDevice, st.stream));
     return TCB_OK;
   }
@@ -174,6 +175,7 @@ int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const d
   }
   const int sms = num_sms();
   if (p.rank == 1 && p.sstr[0] == 1) {
+    note_stream_op();
     TCB_CUDA(cudaMemcpyAsync(dst, src, total * 8, cudaMemcpyDeviceToDevice, st.stream));
     return TCB_OK;
   }

@@ -26,6 +26,13 @@ struct ThreadState {
   int64_t last_tiles = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
+  // Programmatic dependent launch: true while the last operation enqueued on
+  // the thread's own stream was a DMMA GEMM writing [pdl_lo, pdl_hi); the next
+  // GEMM may then start its prologue and main loop before that one finishes
+  // (it waits for it before any global write). Every other stream operation
+  // clears it.
+  bool pdl_ok = false;
+  uintptr_t pdl_lo = 0, pdl_hi = 0;
   tcb_gemm_info last_info{};
   std::string err;
 };
@@ -46,7 +53,14 @@ int ensure_init();  // lazily binds device 0 when tcb_init was not called
     cudaError_t e_ = cudaGetLastError();                                     \
     if (e_ != cudaSuccess) return ::tcb::cuda_fail(e_, "kernel launch");     \
     ++::tcb::state().launches;                                               \
+    ::tcb::state().pdl_ok = false;                                           \
   } while (0)
+
+// A non-GEMM operation was enqueued on `stream` (the current one when null).
+inline void note_stream_op(cudaStream_t stream = nullptr) {
+  ThreadState& st = state();
+  if (stream == nullptr || stream == st.stream) st.pdl_ok = false;
+}
 
 // Device-side launchers (implemented in the .cu files).
 int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C);
