@@ -1140,15 +1140,21 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;  // split-K CTAs wait on each other
-  attr[0].val.cooperative = p.splits > 1 ? 1 : 0;
+  // Split-K CTAs wait on each other, so all of them must be resident: the
+  // cooperative attribute guarantees it for a launch on an idle device. Under
+  // programmatic dependent launch (which a cooperative launch would
+  // serialize) residency follows from grid <= SMs at one CTA per SM: the
+  // previous grid's CTAs exit independently of this one, freeing every SM.
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = (p.splits > 1 && !pdl) ? 1 : 0;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, ta, tb, tc);
-  if (e != cudaSuccess && pdl) {  // combination refused: plain stream order
+  if (e != cudaSuccess && pdl) {  // refused: plain (cooperative) stream order
     cudaGetLastError();
+    attr[0].val.cooperative = p.splits > 1 ? 1 : 0;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, p, ta, tb, tc);
   }
