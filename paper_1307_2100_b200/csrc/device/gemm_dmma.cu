@@ -48,6 +48,7 @@ namespace tcb {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int SK_MAX = 160;            // stream-K: most CTAs sharing one launch
 constexpr int NCW = 8;                 // consumer (DMMA) warps
 constexpr int CTHREADS = NCW * 32;     // 256
 constexpr int PTHREADS = 128;          // producer warpgroup
@@ -58,12 +59,13 @@ constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
 constexpr int STAGES_STAGED = 3;       // ring depth when the epilogue is staged
 constexpr int STAGING_BYTES = BM * BN * 8;  // 128 KB: one accumulator tile
 constexpr int TAIL_BYTES = 256 /*barriers*/ + (BM + BN) * 8 /*offset tables*/;
+constexpr int SLOT_BYTES = (SK_MAX + 1) * 4;  // stream-K contributor slots (split variant)
 constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per CTA on sm_100
 // Shared-memory layout: [ring][staging (staged epilogue only)][barriers][tables].
 template <bool STAGED>
 __host__ __device__ constexpr int smem_bytes() {
   return STAGED ? SMEM_LIMIT
-                : STAGES * STAGE_BYTES + TAIL_BYTES + 1024 /*alignment slack*/;
+                : STAGES * STAGE_BYTES + TAIL_BYTES + SLOT_BYTES + 1024 /*alignment slack*/;
 }
 static_assert(STAGES_STAGED * STAGE_BYTES + STAGING_BYTES + TAIL_BYTES + 512 <= SMEM_LIMIT,
               "staged layout must fit with alignment slack");
@@ -99,7 +101,12 @@ struct Params {
   double alpha, beta;
   int alpha_ne1, beta_nz;  // alpha != 1, beta != 0 (decided on the host)
   int tiles_m, tiles_n, splits, kblocks;
-  int64_t units;
+  int64_t units;                // tiles (data-parallel work items)
+  // stream-K (split variant): CTA c owns k-blocks [sk_start[c], sk_start[c+1])
+  // of the flattened (tile, k-block) space, sk_grid CTAs, work = tiles*kblocks
+  int sk_grid;
+  int64_t work;
+  int sk_start[SK_MAX + 1];
   double* ws;
   unsigned* counters;
   unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
@@ -233,12 +240,10 @@ struct Unit {
   int tm, tn, split;
 };
 
-__device__ __forceinline__ Unit decode_unit(const Params& p, int64_t u64) {
-  const unsigned u = static_cast<unsigned>(u64);
-  const unsigned splits = static_cast<unsigned>(p.splits);
+__device__ __forceinline__ Unit decode_unit(const Params& p, int64_t tile) {
+  const unsigned t = static_cast<unsigned>(tile);
   Unit r;
-  r.split = static_cast<int>(u % splits);
-  const unsigned t = u / splits;
+  r.split = 0;
   const unsigned per_batch = static_cast<unsigned>(p.tiles_m) * static_cast<unsigned>(p.tiles_n);
   r.batch = t / per_batch;
   const unsigned tt = t - r.batch * per_batch;
@@ -299,24 +304,75 @@ __device__ __forceinline__ void unit_coords(const MapProg& g, unsigned o, unsign
 }
 
 // ------------------------------------------------------------------ kernel
-// Producer-side iterator over this CTA's (unit, k-block) sequence. All
-// per-unit address math (64-bit divisions) happens once per unit here, in the
-// producer warpgroup, never on the consumer warps.
+// The work of one CTA as segments (tile, k-blocks [kb0, kb1)):
+//   * data-parallel: whole tiles u = blockIdx.x, blockIdx.x + gridDim.x, ...;
+//   * stream-K (split variant, tiles < SMs): the CTA's contiguous share
+//     [sk_start[c], sk_start[c+1]) of the flattened (tile, k-block) space —
+//     at most two segments (shares are shorter than a tile's k-blocks).
+template <bool SK>
+struct SegIter {
+  int64_t u;         // data-parallel: tile index
+  int64_t pos, end;  // stream-K: position in the (tile, k-block) space
+  __device__ __forceinline__ void init(const Params& p) {
+    if (SK) {
+      pos = p.sk_start[blockIdx.x];
+      end = p.sk_start[blockIdx.x + 1];
+    } else {
+      u = blockIdx.x;
+    }
+  }
+  __device__ __forceinline__ bool next(const Params& p, int64_t& tile, int& kb0, int& kb1) {
+    if (SK) {
+      if (pos >= end) return false;
+      tile = pos / p.kblocks;
+      kb0 = static_cast<int>(pos - tile * p.kblocks);
+      kb1 = static_cast<int>(min(static_cast<int64_t>(p.kblocks), kb0 + (end - pos)));
+      pos = tile * p.kblocks + kb1;
+      return true;
+    }
+    if (u >= p.units) return false;
+    tile = u;
+    kb0 = 0;
+    kb1 = p.kblocks;
+    u += gridDim.x;
+    return true;
+  }
+};
+
+// stream-K: the CTA whose share holds position pos (binary search of sk_start)
+__device__ __forceinline__ int sk_owner(const Params& p, int pos) {
+  int lo = 0, hi = p.sk_grid - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.sk_start[mid] <= pos) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Producer-side iterator over this CTA's (segment, k-block) sequence. All
+// per-segment address math happens once per segment here, in the producer
+// warpgroup, never on the consumer warps.
+template <bool SK>
 struct LoadIter {
-  int64_t u;
+  SegIter<SK> it;
   int kb, kb1;
   int m0, n0;            // tile origin (TMA coordinates are int32)
   int64_t oa, ob;        // batch offsets (cp.async path)
-  int ca[5], cb[5];      // TMA: outer + batch coordinates of the unit's tiles
+  int ca[5], cb[5];      // TMA: outer + batch coordinates of the segment's tile
   bool valid;
 
   template <bool USE_TMA>
-  __device__ __forceinline__ void start_unit(const Params& p) {
-    valid = u < p.units;
+  __device__ __forceinline__ void start(const Params& p) {
+    it.init(p);
+    start_seg<USE_TMA>(p);
+  }
+  template <bool USE_TMA>
+  __device__ __forceinline__ void start_seg(const Params& p) {
+    int64_t tile;
+    valid = it.next(p, tile, kb, kb1);
     if (!valid) return;
-    const Unit un = decode_unit(p, u);
-    kb = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
-    kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
+    const Unit un = decode_unit(p, tile);
     m0 = un.tm * BM;
     n0 = un.tn * BN;
     if (USE_TMA) {
@@ -330,10 +386,7 @@ struct LoadIter {
   }
   template <bool USE_TMA>
   __device__ __forceinline__ void advance(const Params& p) {
-    if (++kb == kb1) {
-      u += gridDim.x;
-      start_unit<USE_TMA>(p);
-    }
+    if (++kb == kb1) start_seg<USE_TMA>(p);
   }
 };
 
@@ -349,9 +402,9 @@ __device__ __forceinline__ int k_coord(const MapProg& g, int d, unsigned k0) {
 
 // Issue one k-block of both operands into a stage. TMA: one thread, 5-D maps
 // (lead, other, 3 batch dims). cp.async: the 128 producer threads.
-template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA>
+template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA, typename Iter>
 __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& tmA,
-                                            const CUtensorMap& tmB, const LoadIter& li,
+                                            const CUtensorMap& tmB, const Iter& li,
                                             uint32_t sA, uint32_t full, int ptid) {
   const int k0 = li.kb * BK;
   const uint32_t sB = sA + STAGE_A;
@@ -463,10 +516,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // per-tile output offsets: composite row(m) / col(n) of the tile, -1 = outside C
   int64_t* s_row = reinterpret_cast<int64_t*>(tail + 256);
   int64_t* s_col = s_row + BM;
+  int* s_slot = reinterpret_cast<int*>(s_col + BN);  // stream-K contributor slots
 
   const int tid = threadIdx.x;
   if (tid == 0) {
-    if (tail + TAIL_BYTES > smem_raw + smem_bytes<STAGED>()) __trap();  // alignment slack
+    if (tail + TAIL_BYTES + (STAGED ? 0 : SLOT_BYTES) > smem_raw + smem_bytes<STAGED>()) __trap();
     for (int s = 0; s < NST; ++s) {
       mbar_init(full0 + 8 * s, USE_TMA ? 1 : PTHREADS);
       mbar_init(empty0 + 8 * s, NCW);
@@ -566,9 +620,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     // ============================ producer ============================
     if (USE_TMA && tid != 0) return;
-    LoadIter li;
-    li.u = blockIdx.x;
-    li.template start_unit<USE_TMA>(p);
+    LoadIter<SPLITK> li;
+    li.template start<USE_TMA>(p);
     uint32_t g = 0;
 #pragma unroll 1
     while (li.valid) {
@@ -605,19 +658,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 
   uint32_t gcons = 0;  // k-blocks consumed by this CTA
-  uint32_t tcount = 0;  // tiles finished by this CTA (staging parity)
-  const bool tl = ctid == 0 && blockIdx.x < p.units;
+  uint32_t tcount = 0;  // segments finished by this CTA (staging parity)
+  const bool tl = ctid == 0;
   trace_mark(p, 0, tl);
+  SegIter<SPLITK> segs;
+  segs.init(p);
+  int64_t seg_tile0 = -1, seg_tile1 = -1;  // stream-K: tiles of this CTA's segments
+  int64_t u;
+  int kb0, kb1;
 #pragma unroll 1
-  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++tcount) {
-    // the staged epilogue (never split) needs no unit decode on the consumers
+  for (; segs.next(p, u, kb0, kb1); ++tcount) {
+    // the staged epilogue needs no unit decode on the consumers
     Unit un{};
-    int kb0 = 0, kb1 = p.kblocks;
-    if constexpr (!STAGED) {
-      un = decode_unit(p, u);
-      kb0 = static_cast<int>(static_cast<int64_t>(un.split) * p.kblocks / p.splits);
-      kb1 = static_cast<int>(static_cast<int64_t>(un.split + 1) * p.kblocks / p.splits);
-    }
+    if constexpr (!STAGED) un = decode_unit(p, u);
 
     double acc[8][4][2];
 #pragma unroll
@@ -716,95 +769,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool use_beta = p.beta != 0.0;
 
     if (SPLITK) {
-      // Split-K (cooperative launch: all splits of a tile are co-resident).
-      // 1) every split stores its partial tile in fragment order: value pair
-      //    (acc[im][in][0..1]) of consumer thread t at pair index v*256 + t,
-      //    v = im*4 + in — one coalesced 16-byte store per pair;
-      // 2) the splits meet at a per-tile arrival counter;
-      // 3) split s reduces pairs [s*P/S, (s+1)*P/S) of the tile, summing the S
-      //    partials in split order — bit-reproducible, spread over all S CTAs.
-      const int64_t tile = u / p.splits;
+      // Stream-K: the segment's partial tile goes to workspace slot
+      // 2*cta + segment in fragment order (value pair acc[im][in][0..1] of
+      // consumer thread t at pair index v*256 + t, v = im*4 + in: one
+      // coalesced 16-byte store per pair) and the tile's arrival counter is
+      // bumped; the reductions run after all of this CTA's segments, so no
+      // CTA waits before it has published everything it owes.
       pdl_wait();  // the previous grid may still read the workspace / counters
-      double2* base = reinterpret_cast<double2*>(p.ws) + tile * p.splits * (BM * BN / 2);
-      double2* part = base + un.split * (BM * BN / 2);
+      double2* part = reinterpret_cast<double2*>(p.ws) +
+                      (2 * static_cast<int64_t>(blockIdx.x) + tcount) * (BM * BN / 2);
 #pragma unroll
       for (int im = 0; im < 8; ++im)
 #pragma unroll
         for (int in = 0; in < 4; ++in)
           __stcg(part + (im * 4 + in) * CTHREADS + ctid,
                  make_double2(acc[im][in][0], acc[im][in][1]));
-      // publish: the CTA barrier orders every thread's partial stores before
-      // thread 0, whose gpu-scope release (cumulative) then announces them
+      // the CTA barrier orders every thread's partial stores before thread 0,
+      // whose gpu-scope release (cumulative) then announces them
       consumer_sync();
       if (tcount == 0) trace_mark(p, 3, tl);
-      if (ctid == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + tile)
-                     : "memory");
-        const unsigned target = (p.epoch + 1u) * static_cast<unsigned>(p.splits);
-        unsigned seen;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.counters + tile)
-                       : "memory");
-          if (seen < target) __nanosleep(32);
-        } while (seen < target);
-      }
-      consumer_sync();
-      if (tcount == 0) trace_mark(p, 4, tl);
-      constexpr int PAIRS = BM * BN / 2;
-      const int p0 = PAIRS * un.split / p.splits;
-      const int p1 = PAIRS * (un.split + 1) / p.splits;
-      // Each thread owns up to RED pairs of the slice and issues all their S
-      // partial loads before summing (one L2 round trip, not S).
-      constexpr int RED = 4;
-#pragma unroll 1
-      for (int pb = p0 + ctid; pb < p1; pb += CTHREADS * RED) {
-        double2 sum[RED];
-#pragma unroll
-        for (int i = 0; i < RED; ++i) sum[i] = make_double2(0.0, 0.0);
-#pragma unroll 1
-        for (int sp0 = 0; sp0 < p.splits; sp0 += 4) {
-          double2 v[4][RED];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int i = 0; i < RED; ++i) {
-              const int pi = pb + i * CTHREADS;
-              v[j][i] = (sp0 + j < p.splits && pi < p1)
-                            ? __ldcg(base + (sp0 + j) * PAIRS + pi) : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int i = 0; i < RED; ++i)
-              if (sp0 + j < p.splits) {  // split order 0..S-1
-                sum[i].x += v[j][i].x;
-                sum[i].y += v[j][i].y;
-              }
-        }
-#pragma unroll
-        for (int i = 0; i < RED; ++i) {
-          const int pi = pb + i * CTHREADS;
-          if (pi >= p1) continue;
-          // pair index -> (m, n): v = pi / 256 (im = v/4, in = v%4), thread t = pi % 256
-          const int v = pi >> 8, t = pi & 255;
-          const int tw = t >> 5, tl2 = t & 31;
-          const int m = (tw & 1) * 64 + (v >> 2) * 8 + (tl2 >> 2);
-          const int n = (tw >> 1) * 32 + (v & 3) * 8 + 2 * (tl2 & 3);
-          const int64_t roff = s_row[m];
-          if (roff < 0) continue;
-          const double sv[2] = {sum[i].x, sum[i].y};
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const int64_t coff = s_col[n + jj];
-            if (coff < 0) continue;
-            double* dst = Cb + roff + coff;
-            double vv = p.alpha * sv[jj];
-            if (use_beta) vv += p.beta * *dst;
-            *dst = vv;
-          }
-        }
-      }
-      if (tcount == 0) trace_mark(p, 5, tl);
+      if (ctid == 0)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + u) : "memory");
+      (tcount == 0 ? seg_tile0 : seg_tile1) = u;
       continue;
     }
 
@@ -825,6 +811,113 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       store_tile<true>(acc, Cb, s_row, coff, cok, wm, r, p.alpha, p.beta);
     } else {
       store_tile<false>(acc, Cb, s_row, coff, cok, wm, r, p.alpha, p.beta);
+    }
+  }
+  if constexpr (SPLITK) {
+    // Reduce this CTA's share of each of its tiles — the pairs in proportion
+    // to the k-blocks it computed there — summing the contributors' partials
+    // in contributor (= k) order: bit-reproducible, spread over all of them.
+    constexpr int PAIRS = BM * BN / 2;
+    const bool use_beta = p.beta != 0.0;
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j) {
+      const int64_t t = j == 0 ? seg_tile0 : seg_tile1;
+      if (t < 0) break;
+      const int tk0 = static_cast<int>(t * p.kblocks);
+      const int first = sk_owner(p, tk0);
+      const int S = sk_owner(p, tk0 + p.kblocks - 1) - first + 1;
+      const Unit un = decode_unit(p, t);
+      consumer_sync();  // the previous tile's tables and slots are consumed
+      {
+        const int i = ctid & 127;
+        if (ctid < 128) {
+          const int64_t m = static_cast<int64_t>(un.tm) * BM + i;
+          s_row[i] = m < p.M ? composite(m, p.c_nrow, p.c_row_ext, p.c_row_str) : -1;
+        } else {
+          const int64_t n = static_cast<int64_t>(un.tn) * BN + i;
+          s_col[i] = n < p.N ? composite(n, p.c_ncol, p.c_col_ext, p.c_col_str) : -1;
+        }
+        // workspace slot of contributor i: its first segment holds tile t
+        // unless its share starts in an earlier tile
+        if (ctid < S) {
+          const int c = first + ctid;
+          s_slot[ctid] = 2 * c + (p.sk_start[c] / p.kblocks == t ? 0 : 1);
+        }
+      }
+      int bc[TCB_MAX_DIMS];
+      int64_t oa, ob, oc;
+      batch_offsets(p, un.batch, oa, ob, oc, bc);
+      double* Cb = p.C + oc;
+      if (ctid == 0) {
+        const unsigned target = (p.epoch + 1u) * static_cast<unsigned>(S);
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.counters + t)
+                       : "memory");
+          if (seen < target) __nanosleep(32);
+        } while (seen < target);
+      }
+      consumer_sync();
+      if (j == 0) trace_mark(p, 4, tl);
+      const double2* ws = reinterpret_cast<const double2*>(p.ws);
+      const int lo = max(p.sk_start[blockIdx.x], tk0) - tk0;
+      const int hi = min(p.sk_start[blockIdx.x + 1], tk0 + p.kblocks) - tk0;
+      const int p0 = static_cast<int>(static_cast<int64_t>(PAIRS) * lo / p.kblocks);
+      const int p1 = static_cast<int>(static_cast<int64_t>(PAIRS) * hi / p.kblocks);
+      // Each thread owns up to RED pairs of the slice and issues 4 partial
+      // loads per pair before summing (few L2 round trips, not S).
+      constexpr int RED = 4;
+#pragma unroll 1
+      for (int pb = p0 + ctid; pb < p1; pb += CTHREADS * RED) {
+        double2 sum[RED];
+#pragma unroll
+        for (int i = 0; i < RED; ++i) sum[i] = make_double2(0.0, 0.0);
+#pragma unroll 1
+        for (int sp0 = 0; sp0 < S; sp0 += 4) {
+          double2 v[4][RED];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int64_t base = sp0 + jj < S ? static_cast<int64_t>(s_slot[sp0 + jj]) * PAIRS : 0;
+#pragma unroll
+            for (int i = 0; i < RED; ++i) {
+              const int pi = pb + i * CTHREADS;
+              v[jj][i] = (sp0 + jj < S && pi < p1) ? __ldcg(ws + base + pi)
+                                                   : make_double2(0.0, 0.0);
+            }
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int i = 0; i < RED; ++i)
+              if (sp0 + jj < S) {  // contributor order 0..S-1
+                sum[i].x += v[jj][i].x;
+                sum[i].y += v[jj][i].y;
+              }
+        }
+#pragma unroll
+        for (int i = 0; i < RED; ++i) {
+          const int pi = pb + i * CTHREADS;
+          if (pi >= p1) continue;
+          // pair index -> (m, n): v = pi / 256 (im = v/4, in = v%4), thread t = pi % 256
+          const int v = pi >> 8, tt = pi & 255;
+          const int tw = tt >> 5, tl2 = tt & 31;
+          const int m = (tw & 1) * 64 + (v >> 2) * 8 + (tl2 >> 2);
+          const int n = (tw >> 1) * 32 + (v & 3) * 8 + 2 * (tl2 & 3);
+          const int64_t roff = s_row[m];
+          if (roff < 0) continue;
+          const double sv[2] = {sum[i].x, sum[i].y};
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int64_t coff = s_col[n + jj];
+            if (coff < 0) continue;
+            double* dst = Cb + roff + coff;
+            double vv = p.alpha * sv[jj];
+            if (use_beta) vv += p.beta * *dst;
+            *dst = vv;
+          }
+        }
+      }
+      if (j == 0) trace_mark(p, 5, tl);
     }
   }
   trace_mark(p, 6, tl);
@@ -1268,17 +1361,44 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     return set_error(TCB_EUNSUPPORTED, "gemm: m, n, batch or tile count above 2^31");
   const int sms = num_sms();
 
-  // Split-K when the tile grid leaves most SMs idle (cfg1-type shapes).
-  int splits = 1;
-  if (tiles < sms) {
-    splits = static_cast<int>(std::min<int64_t>(sms / tiles, std::max<int64_t>(1, kblocks / 8)));
-    splits = std::max(1, std::min(splits, 16));
+  // Stream-K when the tile grid leaves SMs idle (cfg1-type shapes): G CTAs
+  // share the W = tiles * kblocks k-blocks in contiguous ranges (>= 4 each,
+  // shorter than a tile, so at most two tile segments per CTA). A range that
+  // crosses a tile boundary is one k-block shorter than its neighbours: its
+  // CTA stores two partial tiles, and the shorter main loop pays for it.
+  const int64_t W = tiles * kblocks;
+  int G = 1;
+  if (tiles < sms && kblocks >= 8 && W < (1LL << 31)) {
+    G = static_cast<int>(std::min<int64_t>({static_cast<int64_t>(sms), W / 4, SK_MAX}));
+    if (G <= tiles) G = 1;
   }
-  p.splits = splits;
-  p.units = tiles * splits;
-
-  if (splits > 1) {
-    const int64_t need = tiles * splits * BM * BN * 8;
+  const bool streamk = G > 1;
+  p.splits = streamk ? 2 : 1;  // > 1: the split (stream-K) kernel variant
+  p.units = tiles;
+  p.work = W;
+  p.sk_grid = G;
+  int splits = 1;  // reported: most contributors of one tile
+  if (streamk) {
+    int64_t pos = 0;
+    p.sk_start[0] = 0;
+    for (int c = 0; c < G; ++c) {
+      int64_t len = (W - pos + (G - c) - 1) / (G - c);
+      if (c + 1 < G && len > 1 && pos / kblocks != (pos + len - 1) / kblocks) --len;
+      pos += len;
+      p.sk_start[c + 1] = static_cast<int>(pos);
+    }
+    for (int c = 0; c < G; ++c)  // a share may touch at most two tiles
+      if ((p.sk_start[c + 1] - 1) / kblocks - p.sk_start[c] / kblocks > 1)
+        return set_error(TCB_EUNSUPPORTED, "gemm: stream-K share spans more than two tiles");
+    for (int64_t t = 0; t < tiles; ++t) {  // contributors per tile
+      int first = 0, last = 0;
+      for (int c = 0; c < G; ++c) {
+        if (p.sk_start[c] <= t * kblocks) first = c;
+        if (p.sk_start[c] <= (t + 1) * kblocks - 1) last = c;
+      }
+      splits = std::max(splits, last - first + 1);
+    }
+    const int64_t need = 2LL * G * BM * BN * 8;  // two segment slots per CTA
     if (need > st.ws_bytes) {
       if (st.ws) cudaFree(st.ws);
       st.ws = nullptr;
@@ -1286,9 +1406,10 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       TCB_CUDA(cudaMalloc(&st.ws, need));
       st.ws_bytes = need;
     }
-    // Per-tile arrival counters grow by `splits` per launch (epoch); they are
-    // re-zeroed whenever the (tiles, splits) shape changes, after a failed
-    // launch, on reallocation and long before they could wrap.
+    // Per-tile arrival counters grow by the tile's contributor count per
+    // launch (epoch); they are re-zeroed whenever (tiles, kblocks, G)
+    // changes, after a failed launch, on reallocation and long before they
+    // could wrap.
     if (tiles > st.counters_n) {
       if (st.counters) cudaFree(st.counters);
       st.counters = nullptr;
@@ -1297,8 +1418,8 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       st.counters_n = tiles;
       st.last_splits = 0;
     }
-    if (st.last_splits != splits || st.last_tiles != tiles ||
-        static_cast<int64_t>(st.epoch + 2) * splits >= (1LL << 31)) {
+    if (st.last_splits != G || st.last_tiles != tiles || st.last_kblocks != kblocks ||
+        static_cast<int64_t>(st.epoch + 2) * G >= (1LL << 31)) {
       note_stream_op();
       TCB_CUDA(cudaMemsetAsync(st.counters, 0, st.counters_n * sizeof(unsigned), st.stream));
       st.epoch = 0;
@@ -1324,12 +1445,12 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   std::memset(&tc, 0, sizeof tc);
   static const bool no_cstore = getenv("TCB_NO_CSTORE") != nullptr;  // diagnostics
   p.c_tma = 0;
-  if (tma && splits == 1 && d.beta == 0.0 && !no_cstore) {
+  if (tma && !streamk && d.beta == 0.0 && !no_cstore) {
     const char* cwhy = nullptr;
     p.c_tma = make_cmap(&tc, &p.pc, C, d, &cwhy) ? 1 : 0;
   }
 
-  const int grid = static_cast<int>(std::min<int64_t>(p.units, sms));
+  const int grid = streamk ? G : static_cast<int>(std::min<int64_t>(tiles, sms));
   // Programmatic dependent launch when the previous operation on our own
   // stream was a GEMM whose output does not overlap this one's operands
   // (read before griddepcontrol.wait). TCB_NO_PDL=1 disables it.
@@ -1388,14 +1509,15 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       fclose(f);
     }
   }
-  if (splits > 1) {
-    ++st.epoch;  // the counters of these tiles now hold epoch*splits
-    st.last_splits = splits;
+  if (streamk) {
+    ++st.epoch;  // each tile's counter now holds epoch * (its contributor count)
+    st.last_splits = G;
     st.last_tiles = tiles;
+    st.last_kblocks = kblocks;
   }
   st.last_info.path = tma ? 0 : 1;
   st.last_info.splits = splits;
-  st.last_info.units = p.units;
+  st.last_info.units = streamk ? W : tiles;
   st.last_info.grid = grid;
   st.last_info.launches = 1;
   return TCB_OK;

@@ -22,8 +22,9 @@ struct ThreadState {
   unsigned* counters = nullptr;   // split-K per-tile arrival counters
   int64_t counters_n = 0;
   unsigned epoch = 0;             // split-K launches since the counters were zeroed
-  int last_splits = 0;             // (tiles, splits) of the last split-K launch
+  int last_splits = 0;             // (G, tiles, kblocks) of the last stream-K launch
   int64_t last_tiles = 0;
+  int64_t last_kblocks = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   // Programmatic dependent launch: true while the last operation enqueued on
