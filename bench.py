@@ -339,8 +339,12 @@ def main() -> int:
                 T.check(dev.tcb_d2h(out_view.ctypes.data, scat.data_ptr(), scat.numel() * 8))
             else:
                 # the public streamed host path: H2D of slab s+1, the contraction of
-                # slab s and the D2H of slab s-1 overlap (pinned buffers)
-                slabs_used = prep.run_streamed(L, R, O, slabs=0)
+                # slab s and the D2H of slab s-1 overlap (pinned buffers); successive
+                # steps are pipelined (step s+1's uploads overlap step s's last
+                # downloads), every step still moves its inputs up and its result down
+                slabs_used = prep.run_streamed(L, R, O, slabs=0, wait=False)
+        if collective is None:
+            prep.sync()  # the last step's result is on the host
         T.check(dev.tcb_timer_stop(C.byref(ms)))
         rounds.append(max_over_ranks(float(ms.value)) / n_e2e)
     e2e_step_ms = statistics.median(rounds)
@@ -370,8 +374,9 @@ def main() -> int:
                 "h2d_bytes_per_step": int((info["left"] + info["right"]) * 8),
                 "d2h_bytes_per_step": int(info["output"] * 8 // (world if collective else 1)),
                 "steps": n_e2e, "rounds_ms_per_step": [round(r, 4) for r in rounds],
-                "api": ("tcf_run_streamed: H2D / DMMA / D2H overlapped over %d slabs "
-                        "(include/tcf.h)" % slabs_used) if collective is None else
+                "api": ("tcf_run_streamed_async: H2D / DMMA / D2H overlapped over %d slabs, "
+                        "successive steps pipelined, tcf_sync at the end (include/tcf.h)"
+                        % slabs_used) if collective is None else
                        "tcf_upload + tcf_run + NCCL reduce-scatter + D2H of the rank's block"},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
                      "peak": round(peak.value, 3), "unit": "TFLOP/s",

@@ -419,7 +419,12 @@ class PreparedContraction {
   /// is smaller than the operand that would have to go up whole, slabs of a
   /// contracted label are streamed instead (both operands by 2-D copies, C
   /// accumulated on the device, downloaded once). Returns the slab count.
-  int run_streamed(const double* left, const double* right, double* out, int slabs = 0);
+  /// With `wait` false the call returns once everything is enqueued: the
+  /// next run_streamed overlaps its uploads with this one's download drain
+  /// (repeated host-to-host contractions); sync() (or any other member)
+  /// completes it, after which `out` holds the result.
+  int run_streamed(const double* left, const double* right, double* out, int slabs = 0,
+                   bool wait = true);
 
   const DeviceRecipe& recipe() const { return recipe_; }
   std::int64_t left_elements() const { return nl_; }
@@ -438,7 +443,7 @@ class PreparedContraction {
   int auto_slabs_ = -1;    // run_streamed's automatic slab count, once decided
   int stream_mode_ = -1;   // run_streamed: 0 output-label slabs, 1 + label: contracted slabs
   int run_streamed_k(const double* left, const double* right, double* out, int slabs,
-                     int label);
+                     int label, bool wait);
   int device_ = 0;
   std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
   double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;

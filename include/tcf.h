@@ -55,6 +55,12 @@ int tcf_download(void* handle, double* out);
  * (tcb_host_register) for overlap. *slabs_used receives the slab count. */
 int tcf_run_streamed(void* handle, const double* left, const double* right, double* out,
                      int slabs, int* slabs_used);
+/* As tcf_run_streamed, but returns once the work is enqueued: a following
+ * call overlaps its uploads with this one's download drain (a stream of
+ * host-to-host contractions). tcf_sync (or any other call on the handle)
+ * completes it; `out` is valid after that. */
+int tcf_run_streamed_async(void* handle, const double* left, const double* right, double* out,
+                           int slabs, int* slabs_used);
 int tcf_sync(void* handle);
 /* info[12]: left, right, output elements; launches of the last run;
  * permuted bytes; m, n, k, batch; flops; number of permutes; device path

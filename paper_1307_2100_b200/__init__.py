@@ -161,11 +161,14 @@ class Prepared:
         self._ok(self._lib.tcf_run_contraction(self._h))
 
     def run_streamed(self, left: np.ndarray, right: np.ndarray, out: np.ndarray,
-                     slabs: int = 0) -> int:
-        """Host-to-host with H2D/compute/D2H overlapped (pinned buffers)."""
+                     slabs: int = 0, wait: bool = True) -> int:
+        """Host-to-host with H2D/compute/D2H overlapped (pinned buffers).
+        wait=False returns once enqueued: the next call overlaps its uploads
+        with this one's download drain; sync() completes it."""
         used = C.c_int()
-        self._ok(self._lib.tcf_run_streamed(self._h, left.ctypes.data, right.ctypes.data,
-                                            out.ctypes.data, slabs, C.byref(used)))
+        fn = self._lib.tcf_run_streamed if wait else self._lib.tcf_run_streamed_async
+        self._ok(fn(self._h, left.ctypes.data, right.ctypes.data, out.ctypes.data, slabs,
+                    C.byref(used)))
         return used.value
 
     def download(self, out: np.ndarray) -> None:

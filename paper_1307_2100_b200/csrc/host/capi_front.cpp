@@ -263,6 +263,17 @@ int tcf_run_streamed(void* handle, const double* left, const double* right, doub
   TCF_GUARD(nullptr, 0)
 }
 
+int tcf_run_streamed_async(void* handle, const double* left, const double* right, double* out,
+                           int slabs, int* slabs_used) {
+  try {
+    const int n =
+        static_cast<Handle*>(handle)->pc->run_streamed(left, right, out, slabs, /*wait=*/false);
+    if (slabs_used) *slabs_used = n;
+    return 0;
+  }
+  TCF_GUARD(nullptr, 0)
+}
+
 int tcf_download(void* handle, double* out) {
   try {
     static_cast<Handle*>(handle)->pc->download(out);

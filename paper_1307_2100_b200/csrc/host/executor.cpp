@@ -274,6 +274,55 @@ int k_stream_label(const ValidatedContraction& v) {
 }  // namespace
 
 
+// Streams and events of the streamed path, created once per prepared
+// contraction (creating them per call costs more than a small slab).
+struct PreparedContraction::Pipes {
+  void* up = nullptr;
+  void* down = nullptr;
+  std::vector<void*> events;
+  std::size_t next = 0;
+  // an asynchronous call's tail: its last contraction and its last download
+  void* compute_done = nullptr;
+  void* down_done = nullptr;
+  bool pending = false;
+  ~Pipes() {
+    if (down) tcb_stream_sync(down);
+    for (void* e : events) tcb_event_destroy(e);
+    if (compute_done) tcb_event_destroy(compute_done);
+    if (down_done) tcb_event_destroy(down_done);
+    tcb_stream_destroy(up);
+    tcb_stream_destroy(down);
+  }
+  // order this call after a pending one: uploads after its contractions (they
+  // overwrite operands those read), contractions after its downloads (they
+  // overwrite the output those read) — so its download drain overlaps this
+  // call's first uploads
+  void follow(void* compute) {
+    if (!pending) return;
+    check(tcb_stream_wait_event(up, compute_done), "event");
+    check(tcb_stream_wait_event(compute, down_done), "event");
+  }
+  // end of a call: wait for it, or leave it pending
+  void finish(void* compute, bool wait) {
+    check(tcb_event_record(compute_done, compute), "event");
+    check(tcb_event_record(down_done, down), "event");
+    if (wait) check(tcb_stream_sync(down), "sync");
+    pending = !wait;
+  }
+  void drain() {
+    if (pending) check(tcb_stream_sync(down), "sync");
+    pending = false;
+  }
+  void* event() {
+    if (next == events.size()) {
+      void* e = nullptr;
+      check(tcb_event_create(&e), "event");
+      events.push_back(e);
+    }
+    return events[next++];
+  }
+};
+
 PreparedContraction::PreparedContraction(const ValidatedContraction& v, int device)
     : v_(v), device_(device) {
   check(tcb_init(device_), "tcb_init");
@@ -328,12 +377,14 @@ std::int64_t PreparedContraction::permuted_bytes() const {
 
 void PreparedContraction::upload(const double* left, const double* right) {
   check(tcb_init(device_), "tcb_init");
+  if (pipes_) pipes_->drain();
   check(tcb_h2d(dl_, left, nl_ * 8), "upload");
   check(tcb_h2d(dr_, right, nr_ * 8), "upload");
 }
 
 void PreparedContraction::run() {
   check(tcb_init(device_), "tcb_init");
+  if (pipes_) pipes_->drain();
   const std::int64_t before = tcb_launch_count();
   run_permutes();
   run_contraction();
@@ -358,39 +409,19 @@ void PreparedContraction::run_contraction() {
 
 void PreparedContraction::download(double* out) {
   check(tcb_init(device_), "tcb_init");
+  if (pipes_) pipes_->drain();
   check(tcb_d2h(out, do_, no_ * 8), "download");
 }
 
 void PreparedContraction::sync() {
   check(tcb_init(device_), "tcb_init");
+  if (pipes_) pipes_->drain();
   check(tcb_sync(), "sync");
 }
 
 
-// Streams and events of the streamed path, created once per prepared
-// contraction (creating them per call costs more than a small slab).
-struct PreparedContraction::Pipes {
-  void* up = nullptr;
-  void* down = nullptr;
-  std::vector<void*> events;
-  std::size_t next = 0;
-  ~Pipes() {
-    for (void* e : events) tcb_event_destroy(e);
-    tcb_stream_destroy(up);
-    tcb_stream_destroy(down);
-  }
-  void* event() {
-    if (next == events.size()) {
-      void* e = nullptr;
-      check(tcb_event_create(&e), "event");
-      events.push_back(e);
-    }
-    return events[next++];
-  }
-};
-
 int PreparedContraction::run_streamed(const double* left, const double* right, double* out,
-                                      int slabs) {
+                                      int slabs, bool wait) {
   check(tcb_init(device_), "tcb_init");
   // Two ways to stream (chosen once): slabs of the output's outermost label
   // (below: the other operand is uploaded whole first, output slabs go down
@@ -413,7 +444,7 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
       if (no_ < other) stream_mode_ = 1 + kl;
     }
   }
-  if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1);
+  if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1, wait);
   // the stream label: outermost output label, outermost mode of its operand
   const auto& outs = v_.spec.output.indices;
   int label = outs.empty() ? -1 : v_.label_index(outs.back().label);
@@ -508,12 +539,15 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     pipes_ = std::make_unique<Pipes>();
     check(tcb_stream_create(&pipes_->up), "stream");
     check(tcb_stream_create(&pipes_->down), "stream");
+    check(tcb_event_create(&pipes_->compute_done), "event");
+    check(tcb_event_create(&pipes_->down_done), "event");
   }
   Pipes& h = *pipes_;
   h.next = 0;
   void* compute = tcb_current_stream();
   void* up = h.up;
   void* down = h.down;
+  h.follow(compute);
   const std::int64_t before = tcb_launch_count();
   // the other operand: whole, first; its permutation (if any) once
   const double* other_host = on_left ? right : left;
@@ -573,7 +607,7 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
           "download");
     e0 += e;
   }
-  check(tcb_stream_sync(down), "sync");
+  h.finish(compute, wait);
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
@@ -583,7 +617,7 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
 // on the copy stream while slab s-1 is contracted; the slab GEMMs accumulate
 // into C on the device (beta = 1 after the first) and C goes down once.
 int PreparedContraction::run_streamed_k(const double* left, const double* right, double* out,
-                                        int slabs, int label) {
+                                        int slabs, int label, bool wait) {
   const LabelInfo& kl = v_.labels[static_cast<std::size_t>(label)];
   const std::int64_t E = kl.extent;
   if (slabs <= 0)  // ~4 MB of operand data per slab, 2..64 slabs
@@ -637,10 +671,13 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     pipes_ = std::make_unique<Pipes>();
     check(tcb_stream_create(&pipes_->up), "stream");
     check(tcb_stream_create(&pipes_->down), "stream");
+    check(tcb_event_create(&pipes_->compute_done), "event");
+    check(tcb_event_create(&pipes_->down_done), "event");
   }
   Pipes& h = *pipes_;
   h.next = 0;
   void* compute = tcb_current_stream();
+  h.follow(compute);
   const std::int64_t before = tcb_launch_count();
   std::int64_t e0 = 0;
   for (int s = 0; s < slabs; ++s) {
@@ -663,7 +700,7 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   check(tcb_event_record(done, compute), "event");
   check(tcb_stream_wait_event(h.down, done), "event");
   check(tcb_memcpy_async(out, do_, no_ * 8, h.down), "download");
-  check(tcb_stream_sync(h.down), "sync");
+  h.finish(compute, wait);
   launches_ = tcb_launch_count() - before;
   return slabs;
 }

@@ -102,6 +102,7 @@ TCF_API = {
     "tcf_run_contraction": (i32, [vp]),
     "tcf_download": (i32, [vp, vp]),
     "tcf_run_streamed": (i32, [vp, vp, vp, vp, i32, C.POINTER(C.c_int)]),
+    "tcf_run_streamed_async": (i32, [vp, vp, vp, vp, i32, C.POINTER(C.c_int)]),
     "tcf_sync": (i32, [vp]),
     "tcf_info": (i32, [vp, P_i64, cp, i64]),
     "tcf_device_ptrs": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),

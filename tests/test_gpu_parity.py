@@ -235,3 +235,34 @@ def test_full_size_scaling_is_exact_and_additive(dev, cfg):
     assert np.array_equal((4.0 * c1).view(np.uint64), c4.view(np.uint64)), cfg
     assert O.rel_frobenius(c12, c1 + c2) <= TOL, cfg
     p.close()
+
+
+@pytest.mark.parametrize("name,e,x", [
+    ("out-label", "C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]", "a=64,b=48,c=37,k=40"),
+    ("k-label", "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=96,j=40,k=512,l=40"),
+])
+def test_streamed_async_calls_pipeline_correctly(dev, name, e, x):
+    """run_streamed(wait=False) back to back with different inputs: each call's
+    result lands in its own host buffer once synced (tc::PreparedContraction::
+    run_streamed; ordering by events between the copy and compute streams)."""
+    p = T.Prepared(e, x)
+    inf = p.info()
+    bufs = []
+    for seed in (1, 3, 5):
+        L = T.seeded(inf["left"], seed)
+        R = T.seeded(inf["right"], seed + 1)
+        out = np.zeros(inf["output"])
+        for a in (L, R, out):
+            T.check(dev.tcb_host_register(a.ctypes.data, a.nbytes))
+        bufs.append((L, R, out))
+    try:
+        for L, R, out in bufs:
+            assert p.run_streamed(L, R, out, slabs=5, wait=False) == 5, name
+        p.sync()
+        for L, R, out in bufs:
+            assert close(out, O.naive(e, x, L, R)), name
+    finally:
+        for trio in bufs:
+            for a in trio:
+                dev.tcb_host_unregister(a.ctypes.data)
+    p.close()
