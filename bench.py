@@ -136,14 +136,6 @@ def shard_extents(cfg: str, world: int, rank: int) -> str:
     return P.shard_contracted(expr, extents, label, world, rank).extents
 
 
-class CudaArray:
-    """Zero-copy view of a device buffer for torch (__cuda_array_interface__)."""
-
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
-                                         "data": (ptr, False), "version": 3}
-
-
 def cpu_reference(expr: str, extents: str, reps: int, workers: int):
     """Times the unmodified reference CPU path (tc::execute, reference backend)
     via oracle/_ref; falls back to our C port of the naive oracle on a slab."""
@@ -246,9 +238,6 @@ def main() -> int:
     expr, full_extents, desc = CONFIGS[cfg]
     mode, label = MODE[cfg]
     extents = shard_extents(cfg, world, rank)
-    if world > 1:
-        # one stream for our kernels and NCCL: ordering without host syncs
-        T.check(dev.tcb_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     peak = C.c_double()
     T.check(dev.tcb_fp64_peak(C.byref(peak)), "tcb_fp64_peak")
 
@@ -261,13 +250,23 @@ def main() -> int:
     if mode == "ksplit" and world > 1:
         if backend != "nccl":
             raise SystemExit("ksplit (cfg5) needs the nccl backend")
+        # the engine's own NCCL communicator (tcb_comm_*, include/tcb.h): rank 0's
+        # unique id goes to the others over the process group; the reduce-scatter
+        # runs on the engine's stream right behind the contraction
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            T.check(dev.tcb_comm_unique_id(uid), "tcb_comm_unique_id")
+        shipped = [bytes(uid) if rank == 0 else None]
+        torch.distributed.broadcast_object_list(shipped, src=0)
+        uid = (C.c_char * 128).from_buffer_copy(shipped[0])
+        comm = C.c_void_p()
+        T.check(dev.tcb_comm_init(world, rank, uid, C.byref(comm)), "tcb_comm_init")
         _, _, optr = prep.device_ptrs()
-        partial = torch.as_tensor(CudaArray(optr, info["output"]), device="cuda")
-        scat = torch.empty(info["output"] // world, dtype=torch.float64, device="cuda")
+        block = info["output"] // world
+        scat = T.DeviceBuffer(block * 8)
 
         def collective():
-            torch.distributed.reduce_scatter_tensor(scat, partial,
-                                                    op=torch.distributed.ReduceOp.SUM)
+            T.check(dev.tcb_reduce_scatter(optr, scat.ptr, block, comm), "tcb_reduce_scatter")
     L = pinned_array(info["left"], dev)
     R = pinned_array(info["right"], dev)
     O = pinned_array(info["output"], dev)
@@ -335,8 +334,8 @@ def main() -> int:
             if collective is not None:
                 prep.upload(L, R)
                 step()
-                out_view = np.empty(scat.numel())
-                T.check(dev.tcb_d2h(out_view.ctypes.data, scat.data_ptr(), scat.numel() * 8))
+                out_view = np.empty(block)
+                T.check(dev.tcb_d2h(out_view.ctypes.data, scat.ptr, block * 8))
             else:
                 # the public streamed host path: H2D of slab s+1, the contraction of
                 # slab s and the D2H of slab s-1 overlap (pinned buffers); successive
@@ -377,7 +376,7 @@ def main() -> int:
                 "api": ("tcf_run_streamed_async: H2D / DMMA / D2H overlapped over %d slabs, "
                         "successive steps pipelined, tcf_sync at the end (include/tcf.h)"
                         % slabs_used) if collective is None else
-                       "tcf_upload + tcf_run + NCCL reduce-scatter + D2H of the rank's block"},
+                       "tcf_upload + tcf_run + tcb_reduce_scatter (NCCL) + D2H of the rank's block"},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
                      "peak": round(peak.value, 3), "unit": "TFLOP/s",
                      "frac": round(achieved / peak.value, 4), "traffic": None,

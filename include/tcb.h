@@ -164,6 +164,24 @@ int tcb_ddot(int64_t k, const double* x, int64_t incx, const double* y, int64_t 
 int tcb_permute(int rank, const int64_t* ext, const int64_t* src_str, const double* src,
                 double* dst);
 
+/* ---- multi-GPU exchange (NCCL over NVLink / NVSwitch) ---------------------
+ * One process per GPU. The K-split partition contracts a
+ * slab of a contracted label on every rank into a full partial C, then one
+ * reduce-scatter leaves rank r with the summed block r of C's outermost label.
+ * NCCL is loaded at run time (libnccl.so.2); without it these return
+ * TCB_ENCCL. Collectives run on the thread's current stream. */
+#define TCB_COMM_ID_BYTES 128
+int tcb_comm_version(int* version);
+/* On one rank; ship the TCB_COMM_ID_BYTES bytes to the others. */
+int tcb_comm_unique_id(void* id);
+/* Collective over the nranks processes (one GPU each, the thread's device). */
+int tcb_comm_init(int nranks, int rank, const void* id, void** comm);
+int tcb_comm_destroy(void* comm);
+/* recv[0..recv_count) = sum over ranks of send[rank*recv_count + i] (fp64). */
+int tcb_reduce_scatter(const double* send, double* recv, int64_t recv_count, void* comm);
+/* recv[0..count) = sum over ranks of send[0..count) (fp64). */
+int tcb_allreduce(const double* send, double* recv, int64_t count, void* comm);
+
 /* ---- timing -------------------------------------------------------------- */
 /* Device-side timing on this thread's stream: tcb_timer_start/stop bracket
  * work; elapsed in milliseconds between the two events. */

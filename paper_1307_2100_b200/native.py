@@ -82,6 +82,12 @@ TCB_API = {
     "tcb_dger": (i32, [i64, i64, f64, vp, i64, vp, i64, vp, i64]),
     "tcb_ddot": (i32, [i64, vp, i64, vp, i64, P_f64]),
     "tcb_permute": (i32, [i32, P_i64, P_i64, vp, vp]),
+    "tcb_comm_version": (i32, [C.POINTER(C.c_int)]),
+    "tcb_comm_unique_id": (i32, [vp]),
+    "tcb_comm_init": (i32, [i32, i32, vp, C.POINTER(vp)]),
+    "tcb_comm_destroy": (i32, [vp]),
+    "tcb_reduce_scatter": (i32, [vp, vp, i64, vp]),
+    "tcb_allreduce": (i32, [vp, vp, i64, vp]),
     "tcb_timer_start": (i32, []),
     "tcb_timer_stop": (i32, [C.POINTER(C.c_float)]),
     "tcb_fp64_peak": (i32, [P_f64]),

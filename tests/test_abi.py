@@ -54,3 +54,12 @@ def test_kernels_are_sm100a_dmma_and_tma():
     assert "UTMALDG" in sass
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", str(T.native.LIB / "libtcb200.so")],
                                        capture_output=True, text=True).stdout
+
+
+def test_nccl_loads_for_the_collectives():
+    """The collective layer loads NCCL at run time (no link-time dependency)."""
+    import ctypes as C
+    import paper_1307_2100_b200 as T
+    v = C.c_int()
+    assert T.native.device().tcb_comm_version(C.byref(v)) == 0
+    assert v.value >= 22700
