@@ -65,7 +65,10 @@ int tcb_event_destroy(void* event);
 int tcb_event_record(void* event, void* stream);
 int tcb_stream_wait_event(void* stream, void* event);
 int tcb_stream_sync(void* stream);
-/* Current stream of this thread (own or caller-set), as void*. */
+/* Current stream of this thread (own or caller-set), as void*. Work the
+ * caller enqueues on it is ordered like any stream work (asking for the
+ * stream turns off the programmatic overlap of the next GEMM with the
+ * previous one). */
 void* tcb_current_stream(void);
 /* Asynchronous copy in any direction on `stream` (NULL: current stream). */
 int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);

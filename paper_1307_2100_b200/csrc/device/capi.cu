@@ -252,6 +252,9 @@ int tcb_stream_sync(void* stream) {
 
 void* tcb_current_stream(void) {
   if (ensure_init() != TCB_OK) return nullptr;
+  // the caller may enqueue its own work on the stream: the next GEMM must not
+  // start before the previous operation ends (no programmatic launch)
+  note_stream_op();
   return state().stream;
 }
 
