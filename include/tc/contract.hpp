@@ -26,6 +26,45 @@ namespace tc {
 enum class Variance : std::uint8_t { Up, Down };
 char variance_char(Variance v);
 
+struct ValidatedContraction;
+struct ExecutionPlan;
+struct ExecutionStats;
+class KernelBackend;
+
+/// Storage allocator of Tensor: large blocks are mapped directly with
+/// transparent huge pages requested (a 128 MB operand faults in 64 times, not
+/// 32768), and elements are default-initialised, so storage that is about to
+/// be overwritten (a downloaded result) is not zero-filled first. Tensor's
+/// own constructors still zero it, as the reference's do.
+template <typename T>
+struct TensorAllocator {
+  using value_type = T;
+  TensorAllocator() = default;
+  template <typename U>
+  TensorAllocator(const TensorAllocator<U>&) {}
+  T* allocate(std::size_t n);
+  void deallocate(T* p, std::size_t n);
+  template <typename U, typename... Args>
+  void construct(U* p, Args&&... args) {
+    if constexpr (sizeof...(Args) == 0) ::new (static_cast<void*>(p)) U;  // default-init
+    else ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+  template <typename U>
+  bool operator==(const TensorAllocator<U>&) const { return true; }
+  template <typename U>
+  bool operator!=(const TensorAllocator<U>&) const { return false; }
+};
+void* tensor_storage_allocate(std::size_t bytes);
+void tensor_storage_free(void* p, std::size_t bytes);
+template <typename T>
+T* TensorAllocator<T>::allocate(std::size_t n) {
+  return static_cast<T*>(tensor_storage_allocate(n * sizeof(T)));
+}
+template <typename T>
+void TensorAllocator<T>::deallocate(T* p, std::size_t n) {
+  tensor_storage_free(p, n * sizeof(T));
+}
+
 /// Dense fp64 tensor, generalized column-major: stride(mode k) = prod of the
 /// extents of modes 0..k-1. Rank 0 holds one scalar.
 class Tensor {
@@ -64,9 +103,16 @@ class Tensor {
  private:
   std::vector<std::int64_t> ext_, str_;
   std::vector<Variance> var_;
-  std::vector<double> buf_;
+  std::vector<double, TensorAllocator<double>> buf_;
   std::string name_ = "t";
   friend std::int64_t stride_of(const Tensor& t, int mode);
+  // storage left uninitialised, for results that are overwritten whole
+  struct Uninit {};
+  Tensor(std::vector<std::int64_t> extents, std::vector<Variance> variance, std::string name,
+         Uninit);
+  friend std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan&,
+                                                   const ValidatedContraction&, const Tensor&,
+                                                   const Tensor&, const KernelBackend&, int);
 };
 
 std::int64_t stride_of(const Tensor& t, int mode);

@@ -54,6 +54,9 @@ int tcb_d2d(void* dst, const void* src, int64_t bytes);
  * (reference operands live in std::vector<double>, include/tc/tensor.hpp:58). */
 int tcb_host_register(void* ptr, int64_t bytes);
 int tcb_host_unregister(void* ptr);
+/* Page-locked host allocation (cudaHostAlloc, portable across devices). */
+int tcb_host_alloc(void** ptr, int64_t bytes);
+int tcb_host_free(void* ptr);
 
 /* Extra streams and events for overlapping copies with compute (the
  * prepared contraction's streamed host-to-host path). Handles are
@@ -65,6 +68,8 @@ int tcb_event_destroy(void* event);
 int tcb_event_record(void* event, void* stream);
 int tcb_stream_wait_event(void* stream, void* event);
 int tcb_stream_sync(void* stream);
+/* Host waits for the last record of `event`. */
+int tcb_event_sync(void* event);
 /* Current stream of this thread (own or caller-set), as void*. Work the
  * caller enqueues on it is ordered like any stream work (asking for the
  * stream turns off the programmatic overlap of the next GEMM with the

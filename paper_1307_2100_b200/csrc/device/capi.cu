@@ -86,11 +86,39 @@ int tcb_init(int device) {
   return TCB_OK;
 }
 
+// Device memory comes from the device's stream-ordered pool with no release
+// threshold: freed blocks stay cached for the next allocation (a prepared
+// contraction's buffers, a tc::execute call's scratch) instead of going back
+// to the driver — cudaMalloc/cudaFree cost milliseconds per call for the
+// reference API's allocate-per-evaluation pattern. Semantics stay those of
+// cudaMalloc/cudaFree: the block is usable on any stream on return, and a
+// free waits for the device first. On exhaustion the pool is trimmed and the
+// allocation retried.
+static cudaMemPool_t device_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev & 63]) {
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return nullptr;
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev & 63] = pool;
+  }
+  return pools[dev & 63];
+}
+
 int tcb_finalize(void) {
   ThreadState& st = state();
   if (st.device < 0) return TCB_OK;
   cudaSetDevice(st.device);
   if (st.stream) cudaStreamSynchronize(st.stream);
+  if (cudaMemPool_t pool = device_pool()) {  // hand cached blocks back to the driver
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
   if (st.ws) cudaFree(st.ws);
   if (st.counters) cudaFree(st.counters);
   if (st.own_stream) cudaStreamDestroy(st.own_stream);
@@ -132,14 +160,25 @@ int tcb_alloc(void** dptr, int64_t bytes) {
   if (!dptr || bytes < 0) return set_error(TCB_EINVAL, "tcb_alloc: bad argument");
   *dptr = nullptr;
   if (bytes == 0) return TCB_OK;
-  TCB_CUDA(cudaMalloc(dptr, static_cast<size_t>(bytes)));
+  cudaMemPool_t pool = device_pool();
+  ThreadState& st = state();
+  cudaError_t e = cudaMallocAsync(dptr, static_cast<size_t>(bytes), st.stream);
+  if (e == cudaErrorMemoryAllocation && pool) {
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(dptr, static_cast<size_t>(bytes), st.stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  TCB_CUDA(cudaStreamSynchronize(st.stream));  // usable on every stream, like cudaMalloc
   return TCB_OK;
 }
 
 int tcb_free(void* dptr) {
   if (!dptr) return TCB_OK;
   TCB_TRY_INIT();
-  TCB_CUDA(cudaFree(dptr));
+  TCB_CUDA(cudaDeviceSynchronize());  // cudaFree's implicit synchronisation
+  TCB_CUDA(cudaFreeAsync(dptr, state().stream));
   return TCB_OK;
 }
 
@@ -229,6 +268,29 @@ int tcb_event_destroy(void* event) {
 
 static cudaStream_t stream_or_current(void* s) {
   return s ? static_cast<cudaStream_t>(s) : state().stream;
+}
+
+int tcb_event_sync(void* event) {
+  TCB_TRY_INIT();
+  if (!event) return set_error(TCB_EINVAL, "tcb_event_sync: null event");
+  TCB_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(event)));
+  return TCB_OK;
+}
+
+int tcb_host_alloc(void** ptr, int64_t bytes) {
+  TCB_TRY_INIT();
+  if (!ptr || bytes < 0) return set_error(TCB_EINVAL, "tcb_host_alloc: bad argument");
+  *ptr = nullptr;
+  if (bytes == 0) return TCB_OK;
+  TCB_CUDA(cudaHostAlloc(ptr, static_cast<size_t>(bytes), cudaHostAllocPortable));
+  return TCB_OK;
+}
+
+int tcb_host_free(void* ptr) {
+  if (!ptr) return TCB_OK;
+  TCB_TRY_INIT();
+  TCB_CUDA(cudaFreeHost(ptr));
+  return TCB_OK;
 }
 
 int tcb_event_record(void* event, void* stream) {

@@ -6,6 +6,7 @@
 // device launch through the C-ABI (tcb.h). Host C++ only: no CUDA headers.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -13,6 +14,7 @@
 #include <mutex>
 
 #include "tc/contract.hpp"
+#include "staging.hpp"
 #include "tcb.h"
 
 namespace tc {
@@ -378,8 +380,8 @@ std::int64_t PreparedContraction::permuted_bytes() const {
 void PreparedContraction::upload(const double* left, const double* right) {
   check(tcb_init(device_), "tcb_init");
   if (pipes_) pipes_->drain();
-  check(tcb_h2d(dl_, left, nl_ * 8), "upload");
-  check(tcb_h2d(dr_, right, nr_ * 8), "upload");
+  host_to_device(dl_, left, nl_ * 8, nullptr);
+  host_to_device(dr_, right, nr_ * 8, nullptr);
 }
 
 void PreparedContraction::run() {
@@ -410,7 +412,7 @@ void PreparedContraction::run_contraction() {
 void PreparedContraction::download(double* out) {
   check(tcb_init(device_), "tcb_init");
   if (pipes_) pipes_->drain();
-  check(tcb_d2h(out, do_, no_ * 8), "download");
+  device_to_host(out, do_, no_ * 8, nullptr);
 }
 
 void PreparedContraction::sync() {
@@ -731,15 +733,29 @@ std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
                                 "' has no device path; use tc::make_backend(\"b200\")");
 
   const auto t0 = std::chrono::steady_clock::now();
-  Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name);
+  // TC_EXEC_TRACE=1: phase times of this call on stderr (diagnostics)
+  static const bool trace = std::getenv("TC_EXEC_TRACE") != nullptr;
+  auto mark = [&](const char* what) {
+    if (trace)
+      std::fprintf(stderr, "execute %-10s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                             t0).count());
+  };
+  Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name,
+             Tensor::Uninit{});  // overwritten whole by the download
+  mark("output");
   ExecutionStats st;
   st.flops = plan.flops;
   try {
     dev->tick("execute");
     PreparedContraction pc(v, dev->options().device);
+    mark("prepare");
     pc.upload(left.data(), right.data());
+    mark("upload");
     pc.run();
+    mark("run");
     pc.download(out.data());
+    mark("download");
     st.kernel_calls = pc.launches_last_run();
     st.packed_bytes = pc.permuted_bytes();
   } catch (const std::invalid_argument&) {

@@ -61,6 +61,9 @@ TCB_API = {
     "tcb_d2d": (i32, [vp, vp, i64]),
     "tcb_host_register": (i32, [vp, i64]),
     "tcb_host_unregister": (i32, [vp]),
+    "tcb_host_alloc": (i32, [C.POINTER(vp), i64]),
+    "tcb_host_free": (i32, [vp]),
+    "tcb_event_sync": (i32, [vp]),
     "tcb_stream_create": (i32, [C.POINTER(vp)]),
     "tcb_stream_destroy": (i32, [vp]),
     "tcb_event_create": (i32, [C.POINTER(vp)]),
