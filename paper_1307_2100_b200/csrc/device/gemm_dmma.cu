@@ -627,8 +627,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     while (li.valid) {
       const uint32_t s = g % NST;
       mbar_wait(empty0 + 8 * s, ((g / NST) & 1) ^ 1);
-      issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
-                                               full0 + 8 * s, tid);
+      if (USE_TMA && (p.diag & 8) && g >= static_cast<uint32_t>(NST))
+        mbar_arrive(full0 + 8 * s);  // TCB_DIAG bit 8 (timing experiment): no reload
+      else
+        issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
+                                                 full0 + 8 * s, tid);
       ++g;
       li.template advance<USE_TMA>(p);
     }
@@ -682,12 +685,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int kb = kb0; kb < kb1; ++kb) {
       const uint32_t stage = gcons % NST;
       mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
-      if (kb == kb0 && tcount > 0 && tcount <= 8)
-        trace_mark(p, 10 + 3 * (static_cast<int>(tcount) - 1), tl);
-      if (gcons == 0) trace_mark(p, 1, tl);
-      if (gcons == 8) trace_mark(p, 7, tl);
-      if (tcount == 2 && kb == kb0 + 4) trace_mark(p, 30, tl);
-      if (tcount == 2 && kb == kb0 + 8) trace_mark(p, 31, tl);
+      if (p.trace != nullptr) {  // diagnostics only: one uniform branch per k-block
+        if (kb == kb0 && tcount > 0 && tcount <= 8)
+          trace_mark(p, 10 + 3 * (static_cast<int>(tcount) - 1), tl);
+        if (gcons == 0) trace_mark(p, 1, tl);
+        if (gcons == 8) trace_mark(p, 7, tl);
+        if (tcount == 2 && kb == kb0 + 4) trace_mark(p, 30, tl);
+        if (tcount == 2 && kb == kb0 + 8) trace_mark(p, 31, tl);
+      }
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
