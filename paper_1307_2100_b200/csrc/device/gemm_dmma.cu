@@ -503,16 +503,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   constexpr bool STAGED = USE_TMA && !SPLITK;
   constexpr int NST = STAGED ? STAGES_STAGED : STAGES;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1024-aligned base (128B-swizzled TMA boxes) computed in the 32-bit shared
+  // window: the main loop's barrier / stage addresses then rematerialise from
+  // constants instead of re-deriving a generic pointer (S2R of the shared
+  // window) every k-block
+  const uint32_t raw = smem_u32(smem_raw);
+  uint32_t s_base = (raw + 1023u) & ~1023u;
+  asm volatile("mov.b32 %0, %0;" : "+r"(s_base));  // opaque: kept in a register
+  unsigned char* smem = smem_raw + (s_base - raw);
   double* staging = reinterpret_cast<double*>(smem + NST * STAGE_BYTES);
   unsigned char* tail = smem + NST * STAGE_BYTES + (STAGED ? STAGING_BYTES : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(tail);
-  const uint32_t s_base = smem_u32(smem);
-  const uint32_t full0 = smem_u32(bars);         // full[s]  = full0 + 8s
-  const uint32_t empty0 = smem_u32(bars + NST);  // empty[s] = empty0 + 8s
-  const uint32_t stg_full = smem_u32(bars + 2 * NST);       // staging holds a tile
-  const uint32_t stg_empty = smem_u32(bars + 2 * NST + 1);  // staging drained
+  const uint32_t tail_u32 = s_base + NST * STAGE_BYTES + (STAGED ? STAGING_BYTES : 0);
+  const uint32_t full0 = tail_u32;                 // full[s]  = full0 + 8s
+  const uint32_t empty0 = tail_u32 + 8 * NST;      // empty[s] = empty0 + 8s
+  const uint32_t stg_full = tail_u32 + 16 * NST;   // staging holds a tile
+  const uint32_t stg_empty = stg_full + 8;         // staging drained
   // per-tile output offsets: composite row(m) / col(n) of the tile, -1 = outside C
   int64_t* s_row = reinterpret_cast<int64_t*>(tail + 256);
   int64_t* s_col = s_row + BM;
