@@ -7,9 +7,14 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int LOADS>
+template <int LOADS, int BARRIER = 0>
 __global__ void __launch_bounds__(256, 1) mix(double* out, int iters) {
   __shared__ double sm[4096];
+  __shared__ unsigned long long bar[2];
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(&bar[0]))), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(&bar[1]))), "r"((1 << 20) - 1));
+  }
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = 1.0 + i * 1e-9;
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -19,7 +24,20 @@ __global__ void __launch_bounds__(256, 1) mix(double* out, int iters) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(sm)) + lane * 8;
+  const unsigned b0 = static_cast<unsigned>(__cvta_generic_to_shared(&bar[0]));
+  const unsigned b1 = static_cast<unsigned>(__cvta_generic_to_shared(&bar[1]));
   for (int it = 0; it < iters; ++it) {
+    if (BARRIER && (it & 3) == 0) {
+      // the consumer's per-k-block handshake: wait on a completed phase,
+      // then (lane 0) arrive on a barrier that never completes
+      asm volatile(
+          "{\n .reg .pred p;\n"
+          "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n"
+          ::"r"(b0), "r"(1) : "memory");
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b1) : "memory");
+    }
     double a[8], b[4];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -46,18 +64,21 @@ __global__ void __launch_bounds__(256, 1) mix(double* out, int iters) {
   if (s == 1234.5) out[threadIdx.x] = s;
 }
 
-template <int LOADS>
+template <int LOADS, int BARRIER = 0>
 void run(const char* name, int nsm, double* out) {
   const int iters = 20000;
-  mix<LOADS><<<nsm, 256>>>(out, 100);
-  cudaDeviceSynchronize();
+  mix<LOADS, BARRIER><<<nsm, 256>>>(out, 100);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    printf("{\"case\": \"%s\", \"error\": \"%s\"}\n", name, cudaGetErrorString(cudaGetLastError()));
+    return;
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
   for (int r = 0; r < 5; ++r) {
     cudaEventRecord(e0);
-    mix<LOADS><<<nsm, 256>>>(out, iters);
+    mix<LOADS, BARRIER><<<nsm, 256>>>(out, iters);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -75,5 +96,6 @@ int main() {
   cudaMalloc(&out, 1 << 20);
   run<0>("32 DMMA per k-step, no loads", nsm, out);
   run<1>("32 DMMA + 12 LDS.64 per k-step", nsm, out);
+  run<1, 1>("... + mbarrier wait/arrive every 4 k-steps", nsm, out);
   return 0;
 }
