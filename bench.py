@@ -11,11 +11,17 @@ launch). Prints ONE JSON line on rank 0.
 
   value    GFLOP/s, operands resident in HBM, CUDA-event timed over exactly K
            steps, max over ranks; flops = plan.flops = 2*prod(extents).
-  e2e      the same metric through the public plan-level API (tcf_upload ->
-           tcf_run -> tcf_download) with pinned HOST buffers, H2D/D2H inside
-           the timed region.
+           Consecutive steps use programmatic dependent launch (the next
+           contraction's prologue and main loop overlap the previous one's
+           tail; TCB_NO_PDL=1 disables it).
+  e2e      the same metric through the public plan-level API with pinned HOST
+           buffers, every step's H2D of its inputs and D2H of its result inside
+           the timed region: tcf_run_streamed_async (slabs overlapping H2D /
+           DMMA / D2H, successive steps pipelined, tcf_sync at the end); the
+           K-split (cfg5, N>1) uses upload + run + tcb_reduce_scatter + D2H.
   roofline the DMMA GEMM kernel alone (CUDA events on its own stream) against
-           the fp64 DMMA peak measured live on this GPU (tcb_fp64_peak).
+           the fp64 DMMA peak measured live on this GPU (tcb_fp64_peak);
+           traffic = DRAM bytes per launch from profiles/ncu_<cfg>_summary.json.
   cpu_baseline the unmodified reference (oracle/_ref, compiled from
            /root/reference) on the host cores, rank 0, N=1 only.
 
