@@ -513,7 +513,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   unsigned char* smem = smem_raw + (s_base - raw);
   double* staging = reinterpret_cast<double*>(smem + NST * STAGE_BYTES);
   unsigned char* tail = smem + NST * STAGE_BYTES + (STAGED ? STAGING_BYTES : 0);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tail);
   const uint32_t tail_u32 = s_base + NST * STAGE_BYTES + (STAGED ? STAGING_BYTES : 0);
   const uint32_t full0 = tail_u32;                 // full[s]  = full0 + 8s
   const uint32_t empty0 = tail_u32 + 8 * NST;      // empty[s] = empty0 + 8s
