@@ -1,5 +1,5 @@
 // k1/k2 — fp64 GEMM on the B200 DMMA tensor pipe (mma.sync f64 -> SASS
-// DMMA.8x8x4), TMA + mbarrier staging, persistent CTAs, deterministic split-K.
+// DMMA.8x8x4), TMA + mbarrier staging, persistent CTAs, deterministic stream-K.
 //
 // Replaces the reference's ReferenceBackend::gemm (src/kernels_reference.cpp:
 // 33-79) *and* the loop-over-GEMM nest around it (src/executor.cpp:119-177):
@@ -13,24 +13,31 @@
 //     warpgroup. setmaxnreg hands the producer's registers to the consumers
 //     (40 vs 232 per thread): without it a 12-warp CTA caps at 168 registers
 //     and the accumulators spill.
-//   * 6-stage smem ring (32 KB/stage) with full/empty mbarriers. The producer
-//     issues cp.async.bulk.tensor (TMA, 128B swizzle, 5-D maps carrying the
-//     batch dims) from one thread when both operands are TMA-legal, else its
-//     128 threads issue zero-filling 8-byte cp.async arriving on the same
-//     mbarrier.
+//   * smem ring of 32 KB stages with full/empty mbarriers (3 stages next to
+//     the 128 KB staging tile, 6 otherwise). One producer thread issues one
+//     cp.async.bulk.tensor (TMA, 128B swizzle) per operand per stage through
+//     5-D maps built from the operand's index groups — composite M / N / K
+//     read in place (recipe L4) — else 128 producer threads issue zero-filling
+//     8-byte cp.async arriving on the same mbarrier.
 //   * Two smem layouts per operand: "MN-major" (outer index contiguous in
-//     global: 8 boxes of 16(outer) x 16(k)) and "K-major" (k contiguous: one box
-//     of 16(k) x 128(outer)); both 128B-swizzled. The k-set of each DMMA k-step
-//     is {0,1,4,5}+{0,2,8,10}[j] instead of 4 consecutive k, which makes the
-//     fragment loads of *both* layouts exactly 2 wavefronts (conflict-free).
-//   * Persistent: grid = min(units, #SMs); the producer runs ahead across
-//     tile boundaries so the next tile's operands land during the epilogue.
-//   * Split-K for small M*N: every split writes its partial tile to a
-//     workspace; the last-arriving CTA sums the partials in split order
-//     (bit-reproducible run to run) and applies alpha/beta.
-//   * Epilogue writes C through composite row/column offsets (index groups),
-//     decoded once per tile into a shared-memory table, so interleaved output
-//     orders need no permutation pass.
+//     global: 8 chunks of 16(outer) x 16(k)) and "K-major" (k contiguous: one
+//     16(k) x 128(outer) box); both 128B-swizzled. The k-set of each DMMA
+//     k-step is {0,1,4,5}+{0,2,8,10}[j] instead of 4 consecutive k, which makes
+//     the fragment loads of *both* layouts exactly 2 wavefronts.
+//   * Persistent: grid = min(tiles, #SMs); the producer runs ahead across
+//     tile boundaries.
+//   * Staged epilogue: consumers drop the accumulators into a swizzled 128 KB
+//     staging tile (the smem image of a TMA box of C) and start the next tile;
+//     one thread writes the tile with a single TMA tensor store (composite
+//     output groups as tensor-map dims), or producer warps 1-3 do plain stores
+//     where C has no such map.
+//   * Stream-K for small tile grids: CTAs share the (tile, k-block) space from
+//     a host-built start table; partial tiles go to a workspace, arrive on a
+//     per-tile counter, and every contributor reduces its proportional share
+//     in k order (bit-reproducible run to run).
+//   * Programmatic dependent launch between consecutive GEMMs on the engine's
+//     stream: the next grid's prologue and main loop overlap this one's tail;
+//     global writes wait for the previous grid (griddepcontrol).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
