@@ -109,9 +109,12 @@ struct Params {
   int alpha_ne1, beta_nz;  // alpha != 1, beta != 0 (decided on the host)
   int tiles_m, tiles_n, splits, kblocks;
   int64_t units;                // tiles (data-parallel work items)
-  // stream-K (split variant): CTA c owns k-blocks [sk_start[c], sk_start[c+1])
-  // of the flattened (tile, k-block) space, sk_grid CTAs, work = tiles*kblocks
+  // stream-K (split variant): tiles [0, dp_tiles) go whole, round robin
+  // (data-parallel phase); then CTA c owns k-blocks [sk_start[c],
+  // sk_start[c+1]) of the flattened (tile, k-block) space (absolute
+  // positions, from dp_tiles * kblocks on); sk_grid CTAs
   int sk_grid;
+  int dp_tiles;
   int64_t work;
   int sk_start[SK_MAX + 1];
   double* ws;
@@ -321,15 +324,21 @@ struct SegIter {
   int64_t u;         // data-parallel: tile index
   int64_t pos, end;  // stream-K: position in the (tile, k-block) space
   __device__ __forceinline__ void init(const Params& p) {
+    u = blockIdx.x;
     if (SK) {
       pos = p.sk_start[blockIdx.x];
       end = p.sk_start[blockIdx.x + 1];
-    } else {
-      u = blockIdx.x;
     }
   }
   __device__ __forceinline__ bool next(const Params& p, int64_t& tile, int& kb0, int& kb1) {
     if (SK) {
+      if (u < p.dp_tiles) {  // data-parallel phase: whole tiles
+        tile = u;
+        kb0 = 0;
+        kb1 = p.kblocks;
+        u += gridDim.x;
+        return true;
+      }
       if (pos >= end) return false;
       tile = pos / p.kblocks;
       kb0 = static_cast<int>(pos - tile * p.kblocks);
@@ -678,7 +687,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   trace_mark(p, 0, tl);
   SegIter<SPLITK> segs;
   segs.init(p);
-  int64_t seg_tile0 = -1, seg_tile1 = -1;  // stream-K: tiles of this CTA's segments
+  int64_t seg_tile0 = -1, seg_tile1 = -1;  // stream-K: tiles of this CTA's partial segments
+  int npart = 0;
   int64_t u;
   int kb0, kb1;
 #pragma unroll 1
@@ -785,7 +795,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     double* Cb = p.C + oc;
     const bool use_beta = p.beta != 0.0;
 
-    if (SPLITK) {
+    if (SPLITK && (kb0 != 0 || kb1 != p.kblocks)) {
       // Stream-K: the segment's partial tile goes to workspace slot
       // 2*cta + segment in fragment order (value pair acc[im][in][0..1] of
       // consumer thread t at pair index v*256 + t, v = im*4 + in: one
@@ -794,7 +804,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // CTA waits before it has published everything it owes.
       pdl_wait();  // the previous grid may still read the workspace / counters
       double2* part = reinterpret_cast<double2*>(p.ws) +
-                      (2 * static_cast<int64_t>(blockIdx.x) + tcount) * (BM * BN / 2);
+                      (2 * static_cast<int64_t>(blockIdx.x) + npart) * (BM * BN / 2);
 #pragma unroll
       for (int im = 0; im < 8; ++im)
 #pragma unroll
@@ -804,10 +814,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // the CTA barrier orders every thread's partial stores before thread 0,
       // whose gpu-scope release (cumulative) then announces them
       consumer_sync();
-      if (tcount == 0) trace_mark(p, 3, tl);
+      if (npart == 0) trace_mark(p, 3, tl);
       if (ctid == 0)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + u) : "memory");
-      (tcount == 0 ? seg_tile0 : seg_tile1) = u;
+      (npart == 0 ? seg_tile0 : seg_tile1) = u;
+      ++npart;
       continue;
     }
 
@@ -854,11 +865,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int64_t n = static_cast<int64_t>(un.tn) * BN + i;
           s_col[i] = n < p.N ? composite(n, p.c_ncol, p.c_col_ext, p.c_col_str) : -1;
         }
-        // workspace slot of contributor i: its first segment holds tile t
-        // unless its share starts in an earlier tile
+        // workspace slot of contributor i: its first partial segment holds
+        // tile t unless its share starts inside an earlier tile (a share that
+        // starts on a tile boundary opens with a whole tile or with t itself)
         if (ctid < S) {
           const int c = first + ctid;
-          s_slot[ctid] = 2 * c + (p.sk_start[c] / p.kblocks == t ? 0 : 1);
+          const int st0 = p.sk_start[c];
+          const bool head_partial = st0 % p.kblocks != 0;
+          s_slot[ctid] = 2 * c + ((head_partial && st0 / p.kblocks != t) ? 1 : 0);
         }
       }
       int bc[TCB_MAX_DIMS];
@@ -1378,42 +1392,68 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     return set_error(TCB_EUNSUPPORTED, "gemm: m, n, batch or tile count above 2^31");
   const int sms = num_sms();
 
-  // Stream-K when the tile grid leaves SMs idle (cfg1-type shapes): G CTAs
-  // share the W = tiles * kblocks k-blocks in contiguous ranges (>= 4 each,
-  // shorter than a tile, so at most two tile segments per CTA). A range that
-  // crosses a tile boundary is one k-block shorter than its neighbours: its
-  // CTA stores two partial tiles, and the shorter main loop pays for it.
-  const int64_t W = tiles * kblocks;
+  // Stream-K when the tile grid does not fill the SMs evenly:
+  //  * tiles < SMs (cfg1-type shapes): G CTAs share all tiles*kblocks
+  //    k-blocks in contiguous ranges (>= 4 each);
+  //  * more tiles, but the last data-parallel wave would leave > 5 % of the
+  //    machine idle (2048x2048: 256 tiles = 1.73 waves of 148): whole tiles
+  //    for the full waves (data-parallel phase), then the remaining tiles'
+  //    k-blocks shared by all G = SMs CTAs.
+  // Shares are shorter than a tile, so a CTA touches at most two tiles of the
+  // shared range; a share that crosses a tile boundary is one k-block shorter
+  // than its neighbours (its CTA stores two partial tiles).
+  const int64_t W_all = tiles * kblocks;
   int G = 1;
-  if (tiles < sms && kblocks >= 8 && W < (1LL << 31)) {
-    G = static_cast<int>(std::min<int64_t>({static_cast<int64_t>(sms), W / 4, SK_MAX}));
-    if (G <= tiles) G = 1;
+  int64_t dp = 0;  // tiles of the data-parallel phase
+  if (kblocks >= 8 && W_all < (1LL << 31)) {
+    if (tiles < sms) {
+      G = static_cast<int>(std::min<int64_t>({static_cast<int64_t>(sms), W_all / 4, SK_MAX}));
+      if (G <= tiles) G = 1;
+    } else if (sms <= SK_MAX) {
+      const int64_t waves = tiles / sms, rem = tiles % sms;
+      if (rem != 0 && static_cast<double>(waves + 1) * sms > 1.05 * static_cast<double>(tiles) &&
+          std::min<int64_t>(sms, rem * kblocks / 4) > rem) {
+        G = sms;
+        dp = waves * sms;
+      }
+    }
   }
+  // CTAs with a share of the shared range (>= 4 k-blocks each); the others
+  // only take data-parallel tiles
+  const int G_sk = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(G, (tiles - dp) * kblocks / 4)));
   const bool streamk = G > 1;
+  const int64_t W = (tiles - dp) * kblocks;  // the shared (stream-K) range
   p.splits = streamk ? 2 : 1;  // > 1: the split (stream-K) kernel variant
   p.units = tiles;
   p.work = W;
   p.sk_grid = G;
+  p.dp_tiles = static_cast<int>(streamk ? dp : 0);
   int splits = 1;  // reported: most contributors of one tile
   if (streamk) {
+    const int64_t base = dp * kblocks;  // table entries are absolute positions
     int64_t pos = 0;
-    p.sk_start[0] = 0;
+    p.sk_start[0] = static_cast<int>(base);
     for (int c = 0; c < G; ++c) {
-      int64_t len = (W - pos + (G - c) - 1) / (G - c);
-      if (c + 1 < G && len > 1 && pos / kblocks != (pos + len - 1) / kblocks) --len;
+      int64_t len = 0;
+      if (c < G_sk) {
+        len = (W - pos + (G_sk - c) - 1) / (G_sk - c);
+        if (c + 1 < G_sk && len > 1 && pos / kblocks != (pos + len - 1) / kblocks) --len;
+      }
       pos += len;
-      p.sk_start[c + 1] = static_cast<int>(pos);
+      p.sk_start[c + 1] = static_cast<int>(base + pos);
     }
     for (int c = 0; c < G; ++c)  // a share may touch at most two tiles
-      if ((p.sk_start[c + 1] - 1) / kblocks - p.sk_start[c] / kblocks > 1)
+      if (p.sk_start[c + 1] > p.sk_start[c] &&
+          (p.sk_start[c + 1] - 1) / kblocks - p.sk_start[c] / kblocks > 1)
         return set_error(TCB_EUNSUPPORTED, "gemm: stream-K share spans more than two tiles");
-    for (int64_t t = 0; t < tiles; ++t) {  // contributors per tile
-      int first = 0, last = 0;
-      for (int c = 0; c < G; ++c) {
-        if (p.sk_start[c] <= t * kblocks) first = c;
-        if (p.sk_start[c] <= (t + 1) * kblocks - 1) last = c;
-      }
-      splits = std::max(splits, last - first + 1);
+    // most contributors of one shared tile (reported), by a two-pointer sweep
+    int c = 0;
+    for (int64_t t = dp; t < tiles; ++t) {
+      while (c + 1 < G && p.sk_start[c + 1] <= t * kblocks) ++c;
+      int last = c;
+      while (last + 1 < G && p.sk_start[last + 1] <= (t + 1) * kblocks - 1) ++last;
+      splits = std::max(splits, last - c + 1);
     }
     const int64_t need = 2LL * G * BM * BN * 8;  // two segment slots per CTA
     if (need > st.ws_bytes) {
@@ -1534,7 +1574,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
   st.last_info.path = tma ? 0 : 1;
   st.last_info.splits = splits;
-  st.last_info.units = streamk ? W : tiles;
+  st.last_info.units = streamk ? dp + W : tiles;
   st.last_info.grid = grid;
   st.last_info.launches = 1;
   return TCB_OK;
