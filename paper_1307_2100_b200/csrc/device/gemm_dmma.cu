@@ -1411,7 +1411,10 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       if (G <= tiles) G = 1;
     } else if (sms <= SK_MAX) {
       const int64_t waves = tiles / sms, rem = tiles % sms;
-      if (rem != 0 && static_cast<double>(waves + 1) * sms > 1.05 * static_cast<double>(tiles) &&
+      // TCB_SK_WASTE: idle-fraction threshold of the hybrid (diagnostics; default 0.05)
+      static const double waste = getenv("TCB_SK_WASTE") ? atof(getenv("TCB_SK_WASTE")) : 0.05;
+      if (rem != 0 &&
+          static_cast<double>(waves + 1) * sms > (1.0 + waste) * static_cast<double>(tiles) &&
           std::min<int64_t>(sms, rem * kblocks / 4) > rem) {
         G = sms;
         dp = waves * sms;

@@ -202,6 +202,21 @@ def test_permute_is_an_exact_copy(dev):
         assert np.array_equal(got, want), (ext, perm)
 
 
+@pytest.mark.parametrize("e_a,e_t,e_r", [(70, 1000, 300), (64, 4096, 80), (33, 97, 4)])
+def test_large_ragged_transpose_is_an_exact_copy(dev, e_a, e_t, e_r):
+    """Unit-stride dims differ (tiled transpose); the first two shapes are
+    large enough for the 64x64 tiles, with ragged edges in both tile dims."""
+    n = e_a * e_t * e_r
+    src = np.arange(n, dtype=np.float64) * 0.5 - 7.0  # source [t, a, r], t fastest
+    d_src, d_dst = D.from_array(src), D(n * 8)
+    ext = (C.c_int64 * 3)(e_a, e_t, e_r)
+    sstr = (C.c_int64 * 3)(e_t, 1, e_t * e_a)
+    T.check(dev.tcb_permute(3, ext, sstr, d_src.ptr, d_dst.ptr))
+    got = d_dst.to_array(n)
+    want = src.reshape(e_r, e_a, e_t).transpose(0, 2, 1).reshape(-1)  # dst [a, t, r]
+    assert np.array_equal(got, want)
+
+
 def test_split_k_is_deterministic(dev):
     # cfg1-shaped GEMM: few tiles -> split-K with last-CTA ordered reduction
     rng = np.random.default_rng(12)
