@@ -1270,7 +1270,8 @@ cudaError_t launch_one(const Params& p, const CUtensorMap& ta, const CUtensorMap
   // serialize) residency follows from grid <= SMs at one CTA per SM: the
   // previous grid's CTAs exit independently of this one, freeing every SM.
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = (p.splits > 1 && !pdl) ? 1 : 0;
+  static const bool no_coop = getenv("TCB_NO_COOP") != nullptr;  // diagnostics
+  attr[0].val.cooperative = (p.splits > 1 && !pdl && !no_coop) ? 1 : 0;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
