@@ -21,7 +21,8 @@ launch). Prints ONE JSON line on rank 0.
            buffers, every step's H2D of its inputs and D2H of its result inside
            the timed region: tcf_run_streamed_async (slabs overlapping H2D /
            DMMA / D2H, successive steps pipelined, tcf_sync at the end); the
-           K-split (cfg5, N>1) uses upload + run + tcb_reduce_scatter + D2H.
+           K-split (cfg5, N>1) uses upload + the fused scatter/reduce (or, with
+           --exchange nccl, run + tcb_reduce_scatter) + D2H of the rank's block.
   roofline the DMMA GEMM kernel alone (CUDA events on its own stream) against
            the fp64 DMMA peak measured live on this GPU (tcb_fp64_peak);
            traffic = DRAM bytes per launch from profiles/ncu_<cfg>_summary.json.
@@ -70,8 +71,9 @@ CONFIGS = {
 # How a config runs on N ranks (BASELINE.json / SURVEY.md §8e):
 #   weak   each rank evaluates its own full-size slab of a free label (no collective)
 #   shard  strong scaling: the free label is split across ranks (no collective; cfg4 splits b)
-#   ksplit strong scaling: the contracted label is split, partial C reduce-scattered over
-#          NCCL along the outermost output label (cfg5: split l, scatter j)
+#   ksplit strong scaling: the contracted label is split, partial C reduce-scattered along
+#          the outermost output label (cfg5: split l, scatter j): by default fused into
+#          the GEMM epilogue over peer memory (--exchange peer), or NCCL after the GEMM
 MODE = {"cfg1": ("weak", "j"), "cfg2": ("weak", "c"), "cfg3": ("weak", "d"),
         "cfg4": ("shard", "b"), "cfg5": ("ksplit", "l")}
 L2_BYTES = 126 * 2**20
@@ -82,8 +84,72 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+def nvml_index(device: int) -> int:
+    """Physical (NVML / nvidia-smi) index of CUDA device `device`."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    ids = [v.strip() for v in vis.split(",") if v.strip()]
+    if device < len(ids) and ids[device].isdigit():
+        return int(ids[device])
+    return device
+
+
+class NvmlClocks:
+    """SM clock + clock-event-reason sampler on a thread (NVML, every ~2 ms),
+    so even a timed region of a few tens of ms holds many samples; one sample
+    is also taken when the region starts and one when it ends."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, device: int):
+        import threading
+        import pynvml as nv
+        nv.nvmlInit()
+        self.nv = nv
+        self.h = nv.nvmlDeviceGetHandleByIndex(nvml_index(device))
+        self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        self.masks = [(n, getattr(nv, c)) for n, c in self.REASONS]
+        self.rows = []
+        self.halt = threading.Event()
+        self.sample()
+        self.thread = threading.Thread(target=self.loop, daemon=True)
+        self.thread.start()
+
+    def sample(self):
+        nv = self.nv
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except nv.NVMLError:
+            return
+        self.rows.append((float(sm), int(bits)))
+
+    def loop(self):
+        while not self.halt.wait(0.002):
+            self.sample()
+
+    def stop(self) -> dict:
+        self.sample()
+        self.halt.set()
+        self.thread.join(timeout=2)
+        rows = list(self.rows)
+        reasons = sorted({n for _, b in rows for n, m in self.masks if b & m})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": self.max_mhz,
+                "samples": len(rows), "reasons": reasons, "sampler": "nvml"}
+
+
+def Clocks(device: int):
+    try:
+        return NvmlClocks(device)
+    except Exception:
+        return SmiClocks(device)
+
+
+class SmiClocks:
+    """nvidia-smi sampler running during the timed region (fallback when NVML
+    is not importable)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -91,6 +157,7 @@ class Clocks:
 
     def __init__(self, device: int):
         self.proc = None
+        device = nvml_index(device)
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -208,6 +275,10 @@ def main() -> int:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="K-split (cfg5, N>1): partial-C blocks written into their owners' "
+                         "receive buffers by the GEMM epilogue over NVLink (peer, fused) or "
+                         "a separate NCCL reduce-scatter after the GEMM (nccl)")
     ap.add_argument("--l2", default="rotate", choices=["rotate", "flush"],
                     help="keeping L2-sized working sets cold: rotate over copies or flush")
     args = ap.parse_args()
@@ -258,9 +329,20 @@ def main() -> int:
     total_flops = flops * world if mode == "weak" else 2 * int(
         np.prod([int(v.split("=")[1]) for v in full_extents.split(",")]))
     collective = None
-    if mode == "ksplit" and world > 1:
+    exchange = None
+    if mode == "ksplit" and world > 1 and args.exchange == "peer":
+        # fused: the GEMM epilogue writes each block of this rank's partial C
+        # into its owner's receive buffer through the peer window (tcb_peer_*),
+        # then each rank sums its received slots (partition.PeerKSplit)
+        block = info["output"] // world
+        scat = T.DeviceBuffer(block * 8)
+        exchange = P.PeerKSplit(dev, world, rank, block, torch.distributed)
+
+        def collective():
+            pass
+    elif mode == "ksplit" and world > 1:
         if backend != "nccl":
-            raise SystemExit("ksplit (cfg5) needs the nccl backend")
+            raise SystemExit("ksplit (cfg5) with --exchange nccl needs the nccl backend")
         # the engine's own NCCL communicator (tcb_comm_*, include/tcb.h): rank 0's
         # unique id goes to the others over the process group; the reduce-scatter
         # runs on the engine's stream right behind the contraction
@@ -317,6 +399,9 @@ def main() -> int:
     rot = [0]
 
     def step():
+        if exchange is not None:
+            exchange.step(prep, scat.ptr)
+            return
         preps[rot[0] % n_rot].run()
         rot[0] += 1
         if collective is not None:
@@ -413,8 +498,11 @@ def main() -> int:
             "parallelism": "single GPU" if world == 1 else {
                 "weak": f"weak: rank r owns its own full-size {label}-slab (no data-path collective)",
                 "shard": f"strong: {label} split {world} ways (no data-path collective)",
-                "ksplit": f"strong: contracted {label} split {world} ways + NCCL reduce-scatter "
-                          f"of partial C over the outermost output label"}[mode],
+                "ksplit": f"strong: contracted {label} split {world} ways; partial C "
+                          f"reduce-scattered over the outermost output label "
+                          + ("fused: GEMM epilogue writes each block into its owner's receive "
+                             "buffer over NVLink (tcb_peer_*), owner sums the slots"
+                             if exchange is not None else "by NCCL after the GEMM")}[mode],
             "rank_extents": extents,
             "l2": ("inputs larger than L2 per step (A+B+C = %.0f MB > 126 MB), steps back to "
                    "back" % (ws_bytes / 2**20)) if not small else
@@ -433,7 +521,10 @@ def main() -> int:
                 "api": ("tcf_run_streamed_async: H2D / DMMA / D2H overlapped over %d slabs, "
                         "successive steps pipelined, tcf_sync at the end (include/tcf.h)"
                         % slabs_used) if collective is None else
-                       "tcf_upload + tcf_run + tcb_reduce_scatter (NCCL) + D2H of the rank's block"},
+                       ("tcf_upload + tcf_run_scattered into the peer window + tcb_peer_reduce"
+                        " + D2H of the rank's block" if exchange is not None else
+                        "tcf_upload + tcf_run + tcb_reduce_scatter (NCCL) + D2H of the rank's "
+                        "block")},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
                      "peak": round(peak.value, 3), "unit": "TFLOP/s",
                      "frac": round(achieved / peak.value, 4), "traffic": None,

@@ -450,6 +450,15 @@ class PreparedContraction {
   /// run_permutes()). Separately callable so the kernels can be timed alone.
   void run_permutes();
   void run_contraction();
+  /// Permutations + the contraction with the output scattered: the output's
+  /// outermost label is split into `parts` equal blocks and block p is
+  /// written at base + p * part_stride (doubles), each block laid out as it
+  /// is inside the output (block p of a column-major output = its elements
+  /// [p*B, (p+1)*B), B = output_elements() / parts). One GEMM launch; with
+  /// `base` inside a tcb_peer_window the epilogue writes every block straight
+  /// into its owner's receive buffer over NVLink (the fused K-split exchange,
+  /// SURVEY §8e). Throws std::invalid_argument when the label does not split.
+  void run_scattered(double* base, int parts, std::int64_t part_stride);
   /// Device -> host copy of the result (synchronous).
   void download(double* out);
   void sync();

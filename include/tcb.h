@@ -190,6 +190,34 @@ int tcb_reduce_scatter(const double* send, double* recv, int64_t recv_count, voi
 /* recv[0..count) = sum over ranks of send[0..count) (fp64). */
 int tcb_allreduce(const double* send, double* recv, int64_t count, void* comm);
 
+/* ---- peer-memory K-split exchange (fused with the contraction) ------------
+ * The same K-split without a separate collective: every rank's GEMM epilogue
+ * writes block o of its partial C straight into rank o's receive buffer over
+ * NVLink / NVSwitch (tc::PreparedContraction::run_scattered, tcf_run_scattered
+ * in tcf.h), then each owner sums its `world` received slots. Replaces the
+ * tcb_reduce_scatter step above for the K-split; no reference
+ * counterpart (the reference is single-process CPU code).
+ *   tcb_peer_alloc: exportable device memory (size a multiple of
+ *     tcb_peer_granularity), zero-filled, mapped locally; *fd is a POSIX file
+ *     descriptor to ship to the other ranks (SCM_RIGHTS), closed by the caller;
+ *   tcb_peer_window: maps n ranks' allocations (all of size `stride`, rank i's
+ *     descriptor fds[i]) back to back at *window + i*stride, readable and
+ *     writable from this device; the caller closes the descriptors;
+ *   tcb_peer_free: unmaps and releases an allocation or a window;
+ *   tcb_peer_signal: after everything already on the stream, stores `epoch`
+ *     (release, system scope) into the uint64 flag [rank] at window + o*stride
+ *     + flag_off for every owner o < world;
+ *   tcb_peer_reduce: waits (acquire) until flags[0..world) >= epoch, then
+ *     out[i] = sum over s = 0..world-1 in order of slots[s*slot_stride + i]. */
+int tcb_peer_granularity(int64_t* bytes);
+int tcb_peer_alloc(int64_t bytes, void** dptr, int* fd);
+int tcb_peer_window(int n, const int* fds, int64_t stride, void** window);
+int tcb_peer_free(void* ptr);
+int tcb_peer_signal(void* window, int64_t stride, int64_t flag_off, int rank, int world,
+                    uint64_t epoch);
+int tcb_peer_reduce(const double* slots, int world, int64_t count, int64_t slot_stride,
+                    double* out, const uint64_t* flags, uint64_t epoch);
+
 /* ---- timing -------------------------------------------------------------- */
 /* Device-side timing on this thread's stream: tcb_timer_start/stop bracket
  * work; elapsed in milliseconds between the two events. */

@@ -49,6 +49,11 @@ int tcf_run(void* handle);
 /* The two halves of tcf_run (for timing the kernels separately). */
 int tcf_run_permutes(void* handle);
 int tcf_run_contraction(void* handle);
+/* Permutations + contraction with the output's outermost label split into
+ * `parts` blocks, block p written at base + p * part_stride (doubles): the
+ * fused K-split exchange when `base` lies in a tcb_peer_window (tcb.h).
+ * tc::PreparedContraction::run_scattered. */
+int tcf_run_scattered(void* handle, double* base, int parts, int64_t part_stride);
 int tcf_download(void* handle, double* out);
 /* Host-to-host evaluation with transfers overlapped with compute
  * (tc::PreparedContraction::run_streamed); host buffers must be page-locked

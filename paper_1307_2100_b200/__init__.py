@@ -160,6 +160,12 @@ class Prepared:
     def run_contraction(self) -> None:
         self._ok(self._lib.tcf_run_contraction(self._h))
 
+    def run_scattered(self, base: int, parts: int, part_stride: int) -> None:
+        """Contraction with the output's outermost label split into `parts`
+        blocks, block p written at device address base + 8 * p * part_stride
+        (the fused K-split exchange when base lies in a peer window)."""
+        self._ok(self._lib.tcf_run_scattered(self._h, base, parts, part_stride))
+
     def run_streamed(self, left: np.ndarray, right: np.ndarray, out: np.ndarray,
                      slabs: int = 0, wait: bool = True) -> int:
         """Host-to-host with H2D/compute/D2H overlapped (pinned buffers).

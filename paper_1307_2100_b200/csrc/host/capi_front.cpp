@@ -253,6 +253,18 @@ int tcf_run_contraction(void* handle) {
   TCF_GUARD(nullptr, 0)
 }
 
+int tcf_run_scattered(void* handle, double* base, int parts, int64_t part_stride) {
+  try {
+    Handle* h = static_cast<Handle*>(handle);
+    h->pc->run_scattered(base, parts, part_stride);
+    tcb_gemm_info info{};
+    tcb_last_gemm_info(&info);
+    h->path = info.path;
+    return 0;
+  }
+  TCF_GUARD(nullptr, 0)
+}
+
 int tcf_run_streamed(void* handle, const double* left, const double* right, double* out,
                      int slabs, int* slabs_used) {
   try {

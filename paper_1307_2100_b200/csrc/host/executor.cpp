@@ -409,6 +409,69 @@ void PreparedContraction::run_contraction() {
   check(tcb_gemm(&d, a, b, do_), "contraction");
 }
 
+static tcb_gemm_desc scattered_desc(const DeviceRecipe& r, std::int64_t no, int parts,
+                             std::int64_t part_stride) {
+  tcb_gemm_desc d = desc_of(r);
+  if (parts < 1) throw std::invalid_argument("run_scattered: parts must be >= 1");
+  if (parts == 1) return d;
+  // The output's outermost label lives at the high end of the output
+  // sub-index with the largest stride (column-major storage).
+  int which = -1, at = -1;  // 0 rows, 1 columns, 2 batch
+  std::int64_t best = -1;
+  auto scan = [&](int w, int n, const std::int64_t* ext, const std::int64_t* str) {
+    for (int i = 0; i < n; ++i)
+      if (ext[i] > 1 && str[i] > best) best = str[i], which = w, at = i;
+  };
+  scan(0, d.c_nrow, d.c_row_ext, d.c_row_str);
+  scan(1, d.c_ncol, d.c_col_ext, d.c_col_str);
+  scan(2, d.nbatch, d.bat_ext, d.bat_sc);
+  if (which < 0) throw std::invalid_argument("run_scattered: the output has no label to split");
+  std::int64_t* ext = which == 0 ? d.c_row_ext : which == 1 ? d.c_col_ext : d.bat_ext;
+  std::int64_t* str = which == 0 ? d.c_row_str : which == 1 ? d.c_col_str : d.bat_sc;
+  int32_t& cnt = which == 0 ? d.c_nrow : which == 1 ? d.c_ncol : d.nbatch;
+  const std::int64_t e = ext[at], s = str[at];
+  // the outermost label's extent: the sub-index spans strides s .. no
+  if (no % s || (no / s) % e || (e * s) != no)
+    throw std::invalid_argument("run_scattered: the output's outermost label is not the top of "
+                                "an output sub-index");
+  const std::int64_t block = no / parts;
+  if (no % parts || block % s)
+    throw std::invalid_argument("run_scattered: the outermost output label's extent must divide "
+                                "evenly into " + std::to_string(parts) + " blocks");
+  if (part_stride < block)
+    throw std::invalid_argument("run_scattered: part stride below the block size");
+  if (cnt >= TCB_MAX_DIMS)
+    throw std::invalid_argument("run_scattered: too many output sub-indices");
+  // sub-index (e, s) -> (e/parts, s) then (parts, part_stride)
+  for (int i = cnt; i > at + 1; --i) {
+    ext[i] = ext[i - 1];
+    str[i] = str[i - 1];
+    if (which == 2) {
+      d.bat_sa[i] = d.bat_sa[i - 1];
+      d.bat_sb[i] = d.bat_sb[i - 1];
+    }
+  }
+  ext[at] = e / parts;
+  ext[at + 1] = parts;
+  str[at + 1] = part_stride;
+  if (which == 2) {  // a batch label also addresses the operands
+    d.bat_sa[at + 1] = d.bat_sa[at] * (e / parts);
+    d.bat_sb[at + 1] = d.bat_sb[at] * (e / parts);
+  }
+  ++cnt;
+  return d;
+}
+
+void PreparedContraction::run_scattered(double* base, int parts, std::int64_t part_stride) {
+  check(tcb_init(device_), "tcb_init");
+  if (pipes_) pipes_->drain();
+  const tcb_gemm_desc d = scattered_desc(recipe_, no_, parts, part_stride);
+  const std::int64_t before = tcb_launch_count();
+  run_permutes();
+  check(tcb_gemm(&d, pl_ ? pl_ : dl_, pr_ ? pr_ : dr_, base), "contraction");
+  launches_ = tcb_launch_count() - before;
+}
+
 void PreparedContraction::download(double* out) {
   check(tcb_init(device_), "tcb_init");
   if (pipes_) pipes_->drain();

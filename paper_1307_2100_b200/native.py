@@ -91,6 +91,12 @@ TCB_API = {
     "tcb_comm_destroy": (i32, [vp]),
     "tcb_reduce_scatter": (i32, [vp, vp, i64, vp]),
     "tcb_allreduce": (i32, [vp, vp, i64, vp]),
+    "tcb_peer_granularity": (i32, [P_i64]),
+    "tcb_peer_alloc": (i32, [i64, C.POINTER(vp), C.POINTER(C.c_int)]),
+    "tcb_peer_window": (i32, [i32, C.POINTER(C.c_int), i64, C.POINTER(vp)]),
+    "tcb_peer_free": (i32, [vp]),
+    "tcb_peer_signal": (i32, [vp, i64, i64, i32, i32, C.c_uint64]),
+    "tcb_peer_reduce": (i32, [vp, i32, i64, i64, vp, vp, C.c_uint64]),
     "tcb_timer_start": (i32, []),
     "tcb_timer_stop": (i32, [C.POINTER(C.c_float)]),
     "tcb_fp64_peak": (i32, [P_f64]),
@@ -109,6 +115,7 @@ TCF_API = {
     "tcf_run": (i32, [vp]),
     "tcf_run_permutes": (i32, [vp]),
     "tcf_run_contraction": (i32, [vp]),
+    "tcf_run_scattered": (i32, [vp, vp, i32, i64]),
     "tcf_download": (i32, [vp, vp]),
     "tcf_run_streamed": (i32, [vp, vp, vp, vp, i32, C.POINTER(C.c_int)]),
     "tcf_run_streamed_async": (i32, [vp, vp, vp, vp, i32, C.POINTER(C.c_int)]),

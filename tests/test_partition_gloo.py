@@ -90,6 +90,43 @@ def test_partitions_world_size_2_gloo():
     assert sorted(results) == [(0, True, True), (1, True, True)]
 
 
+def _fd_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fd = os.memfd_create(f"rank{rank}")
+        os.write(fd, f"payload of rank {rank}".encode())
+        fds = P.exchange_fds(fd, world, rank, dist)
+        os.close(fd)
+        seen = []
+        for f in fds:
+            os.lseek(f, 0, os.SEEK_SET)
+            seen.append(os.read(f, 64).decode())
+            os.close(f)
+        q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_fd_exchange_gloo(world):
+    """Host plumbing of the fused K-split exchange (PeerKSplit): every rank
+    ends up holding every rank's descriptor, indexed by rank (SCM_RIGHTS over
+    Unix sockets; memfd stands in for the exported device allocation)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [f"payload of rank {r}" for r in range(world)]
+    assert results == [(r, want) for r in range(world)]
+
+
 def test_slab_bounds_cover_exactly():
     for n in (1, 7, 64, 512):
         for w in (1, 2, 3, 8):
