@@ -83,6 +83,11 @@ int tcb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * 2-D H2D of SURVEY §8e; cudaMemcpy2DAsync underneath). */
 int tcb_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
                        int64_t width, int64_t height, void* stream);
+/* Synchronous forms of tcb_memcpy2d_async (host -> device, device -> host). */
+int tcb_h2d_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+               int64_t height);
+int tcb_d2h_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+               int64_t height);
 /* *pinned = 1 when `ptr` is page-locked host memory (registered or allocated). */
 int tcb_host_is_pinned(const void* ptr, int* pinned);
 
@@ -223,6 +228,9 @@ int tcb_peer_reduce(const double* slots, int world, int64_t count, int64_t slot_
  * work; elapsed in milliseconds between the two events. */
 int tcb_timer_start(void);
 int tcb_timer_stop(float* ms);
+/* Milliseconds between two recorded events (tcb_event_create/record); waits
+ * for `stop`. */
+int tcb_event_elapsed(void* start, void* stop, float* ms);
 
 /* Measured fp64 tensor-pipe (DMMA) peak of the current device in TFLOP/s —
  * the roofline denominator bench.py reports against. */

@@ -592,6 +592,29 @@ int tcb_timer_stop(float* ms) {
   return TCB_OK;
 }
 
+int tcb_event_elapsed(void* start, void* stop, float* ms) {
+  TCB_TRY_INIT();
+  if (!start || !stop || !ms) return set_error(TCB_EINVAL, "tcb_event_elapsed: null argument");
+  TCB_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(stop)));
+  TCB_CUDA(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start),
+                                static_cast<cudaEvent_t>(stop)));
+  return TCB_OK;
+}
+
+// Synchronous strided copies (the survey's tcb_h2d_2d / tcb_d2h_2d): the
+// 2-D copy on the thread's stream, then a wait for it.
+int tcb_h2d_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+               int64_t height) {
+  const int rc = tcb_memcpy2d_async(dst, dpitch, src, spitch, width, height, nullptr);
+  if (rc != TCB_OK) return rc;
+  TCB_CUDA(cudaStreamSynchronize(state().stream));
+  return TCB_OK;
+}
+int tcb_d2h_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+               int64_t height) {
+  return tcb_h2d_2d(dst, dpitch, src, spitch, width, height);
+}
+
 int64_t tcb_launch_count(void) { return state().launches; }
 void tcb_reset_launch_count(void) { state().launches = 0; }
 

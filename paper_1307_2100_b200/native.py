@@ -97,6 +97,9 @@ TCB_API = {
     "tcb_peer_free": (i32, [vp]),
     "tcb_peer_signal": (i32, [vp, i64, i64, i32, i32, C.c_uint64]),
     "tcb_peer_reduce": (i32, [vp, i32, i64, i64, vp, vp, C.c_uint64]),
+    "tcb_h2d_2d": (i32, [vp, i64, vp, i64, i64, i64]),
+    "tcb_d2h_2d": (i32, [vp, i64, vp, i64, i64, i64]),
+    "tcb_event_elapsed": (i32, [vp, vp, C.POINTER(C.c_float)]),
     "tcb_timer_start": (i32, []),
     "tcb_timer_stop": (i32, [C.POINTER(C.c_float)]),
     "tcb_fp64_peak": (i32, [P_f64]),

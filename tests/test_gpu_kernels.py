@@ -233,3 +233,32 @@ def test_fp64_peak_microbenchmark(dev):
     p = C.c_double()
     T.check(dev.tcb_fp64_peak(C.byref(p)))
     assert 20.0 < p.value < 60.0  # B200: ~37 TFLOP/s measured
+
+
+def test_copy2d_and_event_elapsed(dev):
+    """tcb_h2d_2d / tcb_d2h_2d move a slab of a middle mode (rows of `width`
+    bytes at pitched offsets); tcb_event_elapsed times between two events."""
+    import ctypes as C
+    x = np.arange(64 * 10, dtype=np.float64)  # 64 x 10 column-major
+    d = T.DeviceBuffer(64 * 4 * 8)
+    # rows 8..15 of columns 0..3: 4 copy rows of 8 doubles, source pitch one
+    # column (512 B), device pitch 256 B
+    T.check(dev.tcb_h2d_2d(d.ptr, 256, x.ctypes.data + 8 * 8, 64 * 8, 8 * 8, 4))
+    back = np.zeros(64 * 10)
+    T.check(dev.tcb_d2h_2d(back.ctypes.data + 8 * 8, 64 * 8, d.ptr, 256, 8 * 8, 4))
+    want = np.zeros(64 * 10)
+    for c in range(4):
+        want[c * 64 + 8:c * 64 + 16] = x[c * 64 + 8:c * 64 + 16]
+    assert np.array_equal(back, want)
+    e0, e1 = C.c_void_p(), C.c_void_p()
+    T.check(dev.tcb_event_create(C.byref(e0)))
+    T.check(dev.tcb_event_create(C.byref(e1)))
+    s = dev.tcb_current_stream()
+    T.check(dev.tcb_event_record(e0, s))
+    T.check(dev.tcb_memset0(d.ptr, 64 * 4 * 8))
+    T.check(dev.tcb_event_record(e1, s))
+    ms = C.c_float(-1.0)
+    T.check(dev.tcb_event_elapsed(e0, e1, C.byref(ms)))
+    assert ms.value >= 0.0
+    T.check(dev.tcb_event_destroy(e0))
+    T.check(dev.tcb_event_destroy(e1))
