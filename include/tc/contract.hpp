@@ -496,7 +496,12 @@ class PreparedContraction {
   ValidatedContraction v_;
   bool groups_ok_ = true;  // L4 allowed (cleared if the device refuses it)
   int auto_slabs_ = -1;    // run_streamed's automatic slab count, once decided
-  int stream_mode_ = -1;   // run_streamed: 0 output-label slabs, 1 + label: contracted slabs
+  int stream_mode_ = -1;   // run_streamed: 0 output-label slabs, 1 + label: contracted slabs,
+                           // -2 - label: slabs of a free label by 2-D copies (run_streamed_f)
+  int f_slabs_ = 0;        // run_streamed_f: slab count, decided with the label
+  int pick_free_label(int* slabs) const;
+  int run_streamed_f(const double* left, const double* right, double* out, int slabs,
+                     int label, bool wait);
   int run_streamed_k(const double* left, const double* right, double* out, int slabs,
                      int label, bool wait);
   int device_ = 0;

@@ -228,8 +228,9 @@ int tcb_peer_reduce(const double* slots, int world, int64_t count, int64_t slot_
  * work; elapsed in milliseconds between the two events. */
 int tcb_timer_start(void);
 int tcb_timer_stop(float* ms);
-/* Milliseconds between two recorded events (tcb_event_create/record); waits
- * for `stop`. */
+/* Milliseconds between two recorded timing events (tcb_event_create_timed;
+ * tcb_event_create makes ordering-only events); waits for `stop`. */
+int tcb_event_create_timed(void** event);
 int tcb_event_elapsed(void* start, void* stop, float* ms);
 
 /* Measured fp64 tensor-pipe (DMMA) peak of the current device in TFLOP/s —

@@ -259,6 +259,15 @@ int tcb_event_create(void** event) {
   return TCB_OK;
 }
 
+int tcb_event_create_timed(void** event) {
+  TCB_TRY_INIT();
+  if (!event) return set_error(TCB_EINVAL, "tcb_event_create_timed: null pointer");
+  cudaEvent_t e = nullptr;
+  TCB_CUDA(cudaEventCreate(&e));
+  *event = e;
+  return TCB_OK;
+}
+
 int tcb_event_destroy(void* event) {
   if (!event) return TCB_OK;
   TCB_TRY_INIT();

@@ -493,23 +493,44 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
   // as they complete) or slabs of a contracted label (run_streamed_k: both
   // operands stream, C accumulates on the device and goes down at the end).
   // The one that leaves fewer bytes outside the overlap wins.
-  if (stream_mode_ < 0) {
+  if (stream_mode_ == -1) {
     stream_mode_ = 0;
-    const int kl = recipe_.permutes.empty() ? k_stream_label(v_) : -1;
-    if (kl >= 0) {
-      std::int64_t other = nl_ + nr_;  // unoverlapped bytes of the output-label mode
-      const auto& outs = v_.spec.output.indices;
-      if (!outs.empty()) {
-        const LabelInfo& li = v_.labels[static_cast<std::size_t>(v_.label_index(outs.back().label))];
-        const bool l = li.left_mode >= 0;
-        if ((l ? li.left_mode == v_.left_rank() - 1 : li.right_mode == v_.right_rank() - 1) &&
-            li.extent >= 2)
-          other = l ? nr_ : nl_;
+    // unoverlapped bytes of the output-label mode: the operand uploaded whole
+    std::int64_t other = nl_ + nr_;
+    int outer = -1;  // the output's outermost label when it is its operand's outermost mode
+    const auto& outs = v_.spec.output.indices;
+    if (!outs.empty()) {
+      const int id = v_.label_index(outs.back().label);
+      const LabelInfo& li = v_.labels[static_cast<std::size_t>(id)];
+      const bool l = li.left_mode >= 0;
+      if ((l ? li.left_mode == v_.left_rank() - 1 : li.right_mode == v_.right_rank() - 1) &&
+          li.extent >= 2) {
+        other = l ? nr_ : nl_;
+        outer = id;
       }
-      if (no_ < other) stream_mode_ = 1 + kl;
     }
+    // a free label elsewhere in the tensors whose slabs go up / down by 2-D
+    // copies may leave a smaller operand outside the overlap (cfg4: slabs of
+    // b stream A and C, only B goes up whole — instead of A for the output's
+    // outermost label j)
+    int fs = 0;
+    const int fl = recipe_.permutes.empty() ? pick_free_label(&fs) : -1;
+    if (fl >= 0 && fl != outer) {
+      const LabelInfo& li = v_.labels[static_cast<std::size_t>(fl)];
+      const std::int64_t o = li.left_mode >= 0 ? nr_ : nl_;
+      if (o < other) {
+        other = o;
+        stream_mode_ = -2 - fl;
+        f_slabs_ = fs;
+      }
+    }
+    const int kl = recipe_.permutes.empty() ? k_stream_label(v_) : -1;
+    if (kl >= 0 && no_ < other) stream_mode_ = 1 + kl;
   }
   if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1, wait);
+  if (stream_mode_ <= -2)
+    return run_streamed_f(left, right, out, slabs > 0 ? slabs : f_slabs_, -2 - stream_mode_,
+                          wait);
   // the stream label: outermost output label, outermost mode of its operand
   const auto& outs = v_.spec.output.indices;
   int label = outs.empty() ? -1 : v_.label_index(outs.back().label);
@@ -538,6 +559,9 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
       // the busier copy direction sets the slab size (16 MB of it per slab)
       const std::int64_t bytes = std::max(on_left ? nl_ : nr_, no_) * 8;
       int want = static_cast<int>(std::min<std::int64_t>(64, bytes / slab_bytes()));
+      // two slabs from 8 MB on: the second slab's upload overlaps the first
+      // slab's contraction (cfg1: 16.8 MB of B)
+      if (want < 2 && bytes >= (8LL << 20)) want = 2;
       const std::int64_t E = v_.labels[static_cast<std::size_t>(label)].extent;
       auto tile_eff = [&](std::int64_t e) {
         ValidatedContraction sv = v_;
@@ -669,6 +693,174 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     check(tcb_event_record(done, compute), "event");
     check(tcb_stream_wait_event(down, done), "event");
     check(tcb_memcpy_async(out + e0 * o_elems, do_ + e0 * o_elems, e * o_elems * 8, down),
+          "download");
+    e0 += e;
+  }
+  h.finish(compute, wait);
+  launches_ = tcb_launch_count() - before;
+  return slabs;
+}
+
+// Geometry of `label` in a column-major tensor: (elements below its mode,
+// elements above it); (0, 0) when the tensor does not carry it. which: 0 left,
+// 1 right, 2 output.
+static std::pair<std::int64_t, std::int64_t> label_geom(const ValidatedContraction& v,
+                                                       int label, int which) {
+  std::vector<std::int64_t> ext;
+  int mode = -1;
+  if (which == 2) {
+    const auto& outs = v.spec.output.indices;
+    for (std::size_t m = 0; m < outs.size(); ++m) {
+      const int id = v.label_index(outs[m].label);
+      ext.push_back(v.labels[static_cast<std::size_t>(id)].extent);
+      if (id == label) mode = static_cast<int>(m);
+    }
+  } else {
+    const LabelInfo& li = v.labels[static_cast<std::size_t>(label)];
+    mode = which ? li.right_mode : li.left_mode;
+    const int rank = which ? v.right_rank() : v.left_rank();
+    for (int m = 0; m < rank; ++m)
+      ext.push_back((which ? v.label_at_right_mode(m) : v.label_at_left_mode(m)).extent);
+  }
+  if (mode < 0) return {0, 0};
+  std::int64_t below = 1, above = 1;
+  for (int m = 0; m < static_cast<int>(ext.size()); ++m) {
+    if (m < mode) below *= ext[static_cast<std::size_t>(m)];
+    if (m > mode) above *= ext[static_cast<std::size_t>(m)];
+  }
+  return {below, above};
+}
+
+// The free label run_streamed_f streams (and its slab count), -1 if none: the
+// one whose other operand (uploaded whole before the pipeline starts) is
+// smallest, among labels whose slabs (a) move as 2-D copies of rows of at
+// least 32 KB in the operand carrying them and in the output, (b) keep the
+// GEMM tiles of both slab sizes >= 95 % as full as the whole contraction's,
+// (c) lower to the same recipe kind without permutations.
+int PreparedContraction::pick_free_label(int* slabs_out) const {
+  int best = -1, best_slabs = 0;
+  std::int64_t best_other = 0;
+  const auto& outs = v_.spec.output.indices;
+  for (const auto& ix : outs) {
+    const int id = v_.label_index(ix.label);
+    const LabelInfo& li = v_.labels[static_cast<std::size_t>(id)];
+    const std::int64_t E = li.extent;
+    if (E < 2) continue;
+    const bool on_left = li.left_mode >= 0;
+    const auto [bx, ax] = label_geom(v_, id, on_left ? 0 : 1);
+    const auto [bc, ac] = label_geom(v_, id, 2);
+    const std::int64_t nx = on_left ? nl_ : nr_, other = on_left ? nr_ : nl_;
+    if (best >= 0 && other >= best_other) continue;
+    int want = static_cast<int>(std::clamp<std::int64_t>(std::max(nx, no_) * 8 / slab_bytes(),
+                                                         2, 64));
+    want = static_cast<int>(std::min<std::int64_t>(want, E));
+    if (ax > 1) want = static_cast<int>(std::min<std::int64_t>(want, bx * 8 * E / kMinRow));
+    if (ac > 1) want = static_cast<int>(std::min<std::int64_t>(want, bc * 8 * E / kMinRow));
+    auto slab_ok = [&](std::int64_t e, double full) {
+      ValidatedContraction sv = v_;
+      sv.labels[static_cast<std::size_t>(id)].extent = e;
+      bool ok = groups_ok_;
+      const DeviceRecipe r = lower_checked(sv, &ok, &v_);
+      if (!r.permutes.empty() || r.layout != recipe_.layout) return false;
+      if (r.m == 1 || r.n == 1) return true;
+      const double pm = static_cast<double>((r.m + 127) / 128 * 128);
+      const double pn = static_cast<double>((r.n + 127) / 128 * 128);
+      return static_cast<double>(r.m) * static_cast<double>(r.n) / (pm * pn) >= 0.95 * full;
+    };
+    double full = 1.0;
+    if (recipe_.m > 1 && recipe_.n > 1)
+      full = static_cast<double>(recipe_.m) * static_cast<double>(recipe_.n) /
+             (static_cast<double>((recipe_.m + 127) / 128 * 128) *
+              static_cast<double>((recipe_.n + 127) / 128 * 128));
+    for (; want >= 2; --want) {
+      const std::int64_t lo = E / want, hi = (E + want - 1) / want;
+      if (slab_ok(lo, full) && (hi == lo || slab_ok(hi, full))) break;
+    }
+    if (want < 2) continue;
+    best = id;
+    best_other = other;
+    best_slabs = want;
+  }
+  *slabs_out = best_slabs;
+  return best;
+}
+
+// Streamed evaluation over slabs of free label `label`: the operand not
+// carrying it goes up whole first; slab s of the operand carrying it goes up
+// (one 2-D copy: `above` rows of below*e elements at pitch below*E) while slab
+// s-1 is contracted in place (the slab recipe lowered with the whole tensors'
+// strides) and slab s-2 of the output comes down the same way.
+int PreparedContraction::run_streamed_f(const double* left, const double* right, double* out,
+                                        int slabs, int label, bool wait) {
+  const LabelInfo& li = v_.labels[static_cast<std::size_t>(label)];
+  const std::int64_t E = li.extent;
+  const bool on_left = li.left_mode >= 0;
+  slabs = static_cast<int>(std::clamp<std::int64_t>(slabs, 1, E));
+  int pinned_l = 0, pinned_r = 0, pinned_o = 0;
+  tcb_host_is_pinned(left, &pinned_l);
+  tcb_host_is_pinned(right, &pinned_r);
+  tcb_host_is_pinned(out, &pinned_o);
+  if (slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
+    upload(left, right);
+    run();
+    download(out);
+    return 1;
+  }
+  const auto [bx, ax] = label_geom(v_, label, on_left ? 0 : 1);
+  const auto [bc, ac] = label_geom(v_, label, 2);
+  std::map<std::int64_t, DeviceRecipe> recipes;  // one per distinct slab extent
+  std::vector<std::int64_t> sizes;
+  for (int i = 0; i < slabs; ++i) {
+    const std::int64_t e = E / slabs + (i < E % slabs ? 1 : 0);
+    sizes.push_back(e);
+    if (recipes.count(e)) continue;
+    ValidatedContraction sv = v_;
+    sv.labels[static_cast<std::size_t>(label)].extent = e;
+    bool ok = groups_ok_;
+    DeviceRecipe r = lower_checked(sv, &ok, &v_);
+    if (!r.permutes.empty()) {  // not expected (checked when the label was picked)
+      upload(left, right);
+      run();
+      download(out);
+      return 1;
+    }
+    recipes.emplace(e, std::move(r));
+  }
+  if (!pipes_) {
+    pipes_ = std::make_unique<Pipes>();
+    check(tcb_stream_create(&pipes_->up), "stream");
+    check(tcb_stream_create(&pipes_->down), "stream");
+    check(tcb_event_create(&pipes_->compute_done), "event");
+    check(tcb_event_create(&pipes_->down_done), "event");
+  }
+  Pipes& h = *pipes_;
+  h.next = 0;
+  void* compute = tcb_current_stream();
+  h.follow(compute);
+  const std::int64_t before = tcb_launch_count();
+  double* x_dev = on_left ? dl_ : dr_;
+  const double* x_host = on_left ? left : right;
+  check(tcb_memcpy_async(on_left ? dr_ : dl_, on_left ? right : left, (on_left ? nr_ : nl_) * 8,
+                         h.up),
+        "upload");
+  std::int64_t e0 = 0;
+  for (int s = 0; s < slabs; ++s) {
+    const std::int64_t e = sizes[static_cast<std::size_t>(s)];
+    check(tcb_memcpy2d_async(x_dev + e0 * bx, bx * E * 8, x_host + e0 * bx, bx * E * 8,
+                             bx * e * 8, ax, h.up),
+          "upload");
+    void* ready = h.event();
+    check(tcb_event_record(ready, h.up), "event");
+    check(tcb_stream_wait_event(compute, ready), "event");
+    const tcb_gemm_desc d = desc_of(recipes.at(e));
+    const double* a = on_left ? dl_ + e0 * bx : dl_;
+    const double* b = on_left ? dr_ : dr_ + e0 * bx;
+    check(tcb_gemm(&d, a, b, do_ + e0 * bc), "contraction");
+    void* done = h.event();
+    check(tcb_event_record(done, compute), "event");
+    check(tcb_stream_wait_event(h.down, done), "event");
+    check(tcb_memcpy2d_async(out + e0 * bc, bc * E * 8, do_ + e0 * bc, bc * E * 8, bc * e * 8,
+                             ac, h.down),
           "download");
     e0 += e;
   }

@@ -100,6 +100,7 @@ TCB_API = {
     "tcb_h2d_2d": (i32, [vp, i64, vp, i64, i64, i64]),
     "tcb_d2h_2d": (i32, [vp, i64, vp, i64, i64, i64]),
     "tcb_event_elapsed": (i32, [vp, vp, C.POINTER(C.c_float)]),
+    "tcb_event_create_timed": (i32, [C.POINTER(vp)]),
     "tcb_timer_start": (i32, []),
     "tcb_timer_stop": (i32, [C.POINTER(C.c_float)]),
     "tcb_fp64_peak": (i32, [P_f64]),

@@ -251,8 +251,8 @@ def test_copy2d_and_event_elapsed(dev):
         want[c * 64 + 8:c * 64 + 16] = x[c * 64 + 8:c * 64 + 16]
     assert np.array_equal(back, want)
     e0, e1 = C.c_void_p(), C.c_void_p()
-    T.check(dev.tcb_event_create(C.byref(e0)))
-    T.check(dev.tcb_event_create(C.byref(e1)))
+    T.check(dev.tcb_event_create_timed(C.byref(e0)))
+    T.check(dev.tcb_event_create_timed(C.byref(e1)))
     s = dev.tcb_current_stream()
     T.check(dev.tcb_event_record(e0, s))
     T.check(dev.tcb_memset0(d.ptr, 64 * 4 * 8))

@@ -187,6 +187,12 @@ def test_cfg5_full_size_sampled(dev):
     # contracted label l (2-D copies, C accumulated on the device)
     ("k-streamed", "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=96,j=40,k=512,l=40"),
     ("k-streamed-L4", "C[+a,+b,+c] = A[+a,+k,+c,+l] * B[-k,+b,-l]", "a=32,b=256,c=5,k=16,l=40"),
+    # a free label in the middle of its operand and of the output (2-D copies
+    # of both; run_streamed_f): cfg4's shape streams A and C along b, only the
+    # small B goes up whole
+    ("free-label-left", "C[+a,+b,+i,+j] = A[+a,+b,+k,+l] * B[-k,-l,+i,+j]",
+     "a=512,b=40,i=8,j=6,k=8,l=8"),
+    ("free-label-right", "C[+i,+j,+a] = A[+a,+k] * B[-k,+i,+j]", "a=16,k=64,i=512,j=40"),
 ])
 def test_streamed_host_path_matches(dev, name, e, x):
     # tc::PreparedContraction::run_streamed: slabs of the operand carrying the
