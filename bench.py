@@ -460,6 +460,12 @@ def main() -> int:
     prep.upload(L, R)
     prep.run()
     prep.download(O)
+    if collective is None:
+        # untimed warm-up of the streamed path (its streams, events and second
+        # device buffer set are created on first use)
+        for _ in range(2):
+            prep.run_streamed(L, R, O, slabs=0, wait=False)
+        prep.sync()
     barrier()
     # three timed rounds; the median round is reported (host-side PCIe / page
     # effects make single short rounds noisy), all rounds are listed

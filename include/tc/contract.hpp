@@ -508,6 +508,11 @@ class PreparedContraction {
   std::int64_t nl_ = 0, nr_ = 0, no_ = 0;
   double *dl_ = nullptr, *dr_ = nullptr, *do_ = nullptr;
   double *pl_ = nullptr, *pr_ = nullptr;  // permuted operands (L3)
+  // second buffer set of the pipelined streamed path (flip_buffers)
+  double *dl2_ = nullptr, *dr2_ = nullptr, *do2_ = nullptr, *pl2_ = nullptr, *pr2_ = nullptr;
+  int dbuf_ = -1;  // -1 undecided, 0 one set, 1 two sets
+  int set_ = 0;    // buffer set in use
+  void flip_buffers();
   std::int64_t launches_ = 0;
   struct Pipes;
   std::unique_ptr<Pipes> pipes_;  // streamed path: copy streams + events

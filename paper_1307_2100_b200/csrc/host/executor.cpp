@@ -283,37 +283,55 @@ struct PreparedContraction::Pipes {
   void* down = nullptr;
   std::vector<void*> events;
   std::size_t next = 0;
-  // an asynchronous call's tail: its last contraction and its last download
-  void* compute_done = nullptr;
-  void* down_done = nullptr;
-  bool pending = false;
+  // per device buffer set (two when successive asynchronous calls alternate
+  // between buffer sets): the tail of the last call that used the set — its
+  // last contraction and its last download
+  void* compute_done[2] = {nullptr, nullptr};
+  void* down_done[2] = {nullptr, nullptr};
+  bool pending[2] = {false, false};
+  Pipes() {
+    check(tcb_stream_create(&up), "stream");
+    check(tcb_stream_create(&down), "stream");
+    for (int i = 0; i < 2; ++i) {
+      check(tcb_event_create(&compute_done[i]), "event");
+      check(tcb_event_create(&down_done[i]), "event");
+    }
+  }
   ~Pipes() {
     if (down) tcb_stream_sync(down);
     for (void* e : events) tcb_event_destroy(e);
-    if (compute_done) tcb_event_destroy(compute_done);
-    if (down_done) tcb_event_destroy(down_done);
+    for (int i = 0; i < 2; ++i) {
+      if (compute_done[i]) tcb_event_destroy(compute_done[i]);
+      if (down_done[i]) tcb_event_destroy(down_done[i]);
+    }
     tcb_stream_destroy(up);
     tcb_stream_destroy(down);
   }
-  // order this call after a pending one: uploads after its contractions (they
-  // overwrite operands those read), contractions after its downloads (they
-  // overwrite the output those read) — so its download drain overlaps this
-  // call's first uploads
-  void follow(void* compute) {
-    if (!pending) return;
-    check(tcb_stream_wait_event(up, compute_done), "event");
-    check(tcb_stream_wait_event(compute, down_done), "event");
+  // order this call after the pending one that used buffer set `set`:
+  // uploads after its contractions (they overwrite operands those read),
+  // contractions after its downloads (they overwrite the output those read).
+  // With one set that is the previous call, whose download drain then overlaps
+  // this call's first uploads; with two sets it is the call before that, so
+  // this call's uploads overlap the previous call's contractions as well.
+  void follow(void* compute, int set) {
+    if (!pending[set]) return;
+    check(tcb_stream_wait_event(up, compute_done[set]), "event");
+    check(tcb_stream_wait_event(compute, down_done[set]), "event");
   }
   // end of a call: wait for it, or leave it pending
-  void finish(void* compute, bool wait) {
-    check(tcb_event_record(compute_done, compute), "event");
-    check(tcb_event_record(down_done, down), "event");
-    if (wait) check(tcb_stream_sync(down), "sync");
-    pending = !wait;
+  void finish(void* compute, bool wait, int set) {
+    check(tcb_event_record(compute_done[set], compute), "event");
+    check(tcb_event_record(down_done[set], down), "event");
+    if (wait) {
+      check(tcb_stream_sync(down), "sync");
+      pending[0] = pending[1] = false;
+    } else {
+      pending[set] = true;
+    }
   }
   void drain() {
-    if (pending) check(tcb_stream_sync(down), "sync");
-    pending = false;
+    if (pending[0] || pending[1]) check(tcb_stream_sync(down), "sync");
+    pending[0] = pending[1] = false;
   }
   void* event() {
     if (next == events.size()) {
@@ -369,6 +387,45 @@ PreparedContraction::~PreparedContraction() {
   tcb_free(do_);
   tcb_free(pl_);
   tcb_free(pr_);
+  tcb_free(dl2_);
+  tcb_free(dr2_);
+  tcb_free(do2_);
+  tcb_free(pl2_);
+  tcb_free(pr2_);
+}
+
+// Successive asynchronous streamed calls alternate between two device buffer
+// sets (allocated on the first such call, skipped when they do not fit), so a
+// call's uploads and contractions never wait for the previous call's
+// contractions and downloads — only for those of the call before it.
+void PreparedContraction::flip_buffers() {
+  if (dbuf_ < 0) {
+    dbuf_ = 0;
+    auto grab = [](std::int64_t n) {
+      void* p = nullptr;
+      if (n > 0 && tcb_alloc(&p, n * 8) != TCB_OK) throw std::bad_alloc();
+      return static_cast<double*>(p);
+    };
+    try {
+      dl2_ = grab(nl_);
+      dr2_ = grab(nr_);
+      do2_ = grab(no_);
+      for (const PermuteStep& ps : recipe_.permutes) (ps.right ? pr2_ : pl2_) = grab(ps.elements);
+      dbuf_ = 1;
+    } catch (const std::bad_alloc&) {
+      for (double** q : {&dl2_, &dr2_, &do2_, &pl2_, &pr2_}) {
+        tcb_free(*q);
+        *q = nullptr;
+      }
+    }
+  }
+  if (dbuf_ != 1) return;
+  std::swap(dl_, dl2_);
+  std::swap(dr_, dr2_);
+  std::swap(do_, do2_);
+  std::swap(pl_, pl2_);
+  std::swap(pr_, pr2_);
+  set_ ^= 1;
 }
 
 std::int64_t PreparedContraction::permuted_bytes() const {
@@ -488,6 +545,7 @@ void PreparedContraction::sync() {
 int PreparedContraction::run_streamed(const double* left, const double* right, double* out,
                                       int slabs, bool wait) {
   check(tcb_init(device_), "tcb_init");
+  if (!wait || dbuf_ == 1) flip_buffers();
   // Two ways to stream (chosen once): slabs of the output's outermost label
   // (below: the other operand is uploaded whole first, output slabs go down
   // as they complete) or slabs of a contracted label (run_streamed_k: both
@@ -624,19 +682,13 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     return 1;
   }
 
-  if (!pipes_) {
-    pipes_ = std::make_unique<Pipes>();
-    check(tcb_stream_create(&pipes_->up), "stream");
-    check(tcb_stream_create(&pipes_->down), "stream");
-    check(tcb_event_create(&pipes_->compute_done), "event");
-    check(tcb_event_create(&pipes_->down_done), "event");
-  }
+  if (!pipes_) pipes_ = std::make_unique<Pipes>();
   Pipes& h = *pipes_;
   h.next = 0;
   void* compute = tcb_current_stream();
   void* up = h.up;
   void* down = h.down;
-  h.follow(compute);
+  h.follow(compute, set_);
   const std::int64_t before = tcb_launch_count();
   // the other operand: whole, first; its permutation (if any) once
   const double* other_host = on_left ? right : left;
@@ -696,7 +748,7 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
           "download");
     e0 += e;
   }
-  h.finish(compute, wait);
+  h.finish(compute, wait, set_);
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
@@ -826,17 +878,11 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
     }
     recipes.emplace(e, std::move(r));
   }
-  if (!pipes_) {
-    pipes_ = std::make_unique<Pipes>();
-    check(tcb_stream_create(&pipes_->up), "stream");
-    check(tcb_stream_create(&pipes_->down), "stream");
-    check(tcb_event_create(&pipes_->compute_done), "event");
-    check(tcb_event_create(&pipes_->down_done), "event");
-  }
+  if (!pipes_) pipes_ = std::make_unique<Pipes>();
   Pipes& h = *pipes_;
   h.next = 0;
   void* compute = tcb_current_stream();
-  h.follow(compute);
+  h.follow(compute, set_);
   const std::int64_t before = tcb_launch_count();
   double* x_dev = on_left ? dl_ : dr_;
   const double* x_host = on_left ? left : right;
@@ -864,7 +910,7 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
           "download");
     e0 += e;
   }
-  h.finish(compute, wait);
+  h.finish(compute, wait, set_);
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
@@ -924,17 +970,11 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     }
     recipes.emplace(e, std::move(r));
   }
-  if (!pipes_) {
-    pipes_ = std::make_unique<Pipes>();
-    check(tcb_stream_create(&pipes_->up), "stream");
-    check(tcb_stream_create(&pipes_->down), "stream");
-    check(tcb_event_create(&pipes_->compute_done), "event");
-    check(tcb_event_create(&pipes_->down_done), "event");
-  }
+  if (!pipes_) pipes_ = std::make_unique<Pipes>();
   Pipes& h = *pipes_;
   h.next = 0;
   void* compute = tcb_current_stream();
-  h.follow(compute);
+  h.follow(compute, set_);
   const std::int64_t before = tcb_launch_count();
   std::int64_t e0 = 0;
   for (int s = 0; s < slabs; ++s) {
@@ -957,7 +997,7 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   check(tcb_event_record(done, compute), "event");
   check(tcb_stream_wait_event(h.down, done), "event");
   check(tcb_memcpy_async(out, do_, no_ * 8, h.down), "download");
-  h.finish(compute, wait);
+  h.finish(compute, wait, set_);
   launches_ = tcb_launch_count() - before;
   return slabs;
 }

@@ -246,15 +246,21 @@ def test_full_size_scaling_is_exact_and_additive(dev, cfg):
 @pytest.mark.parametrize("name,e,x", [
     ("out-label", "C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]", "a=64,b=48,c=37,k=40"),
     ("k-label", "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=96,j=40,k=512,l=40"),
+    ("free-label", "C[+a,+b,+i,+j] = A[+a,+b,+k,+l] * B[-k,-l,+i,+j]",
+     "a=512,b=40,i=8,j=6,k=8,l=8"),
+    ("class3", "C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]",
+     "a=24,b=8,c=6,d=10,k=4,l=3"),
 ])
 def test_streamed_async_calls_pipeline_correctly(dev, name, e, x):
     """run_streamed(wait=False) back to back with different inputs: each call's
     result lands in its own host buffer once synced (tc::PreparedContraction::
-    run_streamed; ordering by events between the copy and compute streams)."""
+    run_streamed; ordering by events between the copy and compute streams;
+    successive calls alternate between two device buffer sets, so five calls
+    reuse each set twice or more)."""
     p = T.Prepared(e, x)
     inf = p.info()
     bufs = []
-    for seed in (1, 3, 5):
+    for seed in (1, 3, 5, 7, 9):
         L = T.seeded(inf["left"], seed)
         R = T.seeded(inf["right"], seed + 1)
         out = np.zeros(inf["output"])
