@@ -143,7 +143,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 
 // out[i] = sum_{s=0..world-1} slots[s * slot_stride + i], s in order. Every
-// block first waits until all `world` flags have reached `epoch`.
+// block first waits until all `world` flags have reached `epoch`. HBM-bound
+// (reads world blocks, writes one): each thread keeps two 16-byte elements x
+// four slots of loads in flight before adding them in slot order.
+__device__ __forceinline__ void add2(double2& a, const double2 v) {
+  a.x += v.x;
+  a.y += v.y;
+}
+
 __global__ void __launch_bounds__(256) peer_reduce_kernel(
     const double* __restrict__ slots, int world, int64_t count, int64_t slot_stride,
     double* __restrict__ out, const unsigned long long* flags, unsigned long long epoch) {
@@ -152,17 +159,36 @@ __global__ void __launch_bounds__(256) peer_reduce_kernel(
     while (ld_acquire_sys(f) < epoch) __nanosleep(256);
   }
   __syncthreads();
+  const double2* src = reinterpret_cast<const double2*>(slots);
+  const int64_t ss = slot_stride / 2;  // in double2
   const int64_t n2 = count / 2;
   const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n2;
-       i += step) {
-    double2 acc = __ldcs(reinterpret_cast<const double2*>(slots) + i);
-    for (int s = 1; s < world; ++s) {
-      const double2 v = __ldcs(reinterpret_cast<const double2*>(slots + s * slot_stride) + i);
-      acc.x += v.x;
-      acc.y += v.y;
+       i += 2 * step) {
+    const int64_t j = i + step;
+    const bool two = j < n2;
+    double2 a = __ldcs(src + i);
+    double2 b = two ? __ldcs(src + j) : make_double2(0.0, 0.0);
+    int s = 1;
+    for (; s + 4 <= world; s += 4) {
+      double2 va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        va[u] = __ldcs(src + (s + u) * ss + i);
+        vb[u] = two ? __ldcs(src + (s + u) * ss + j) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        add2(a, va[u]);
+        add2(b, vb[u]);
+      }
     }
-    __stcs(reinterpret_cast<double2*>(out) + i, acc);
+    for (; s < world; ++s) {
+      add2(a, __ldcs(src + s * ss + i));
+      if (two) add2(b, __ldcs(src + s * ss + j));
+    }
+    __stcs(reinterpret_cast<double2*>(out) + i, a);
+    if (two) __stcs(reinterpret_cast<double2*>(out) + j, b);
   }
   if (count & 1) {
     const int64_t i = count - 1;
@@ -325,7 +351,7 @@ int tcb_peer_reduce(const double* slots, int world, int64_t count, int64_t slot_
                      "tcb_peer_reduce: bad arguments (16-byte aligned slots/out, even slot "
                      "stride >= count, 1 <= world <= 256)");
   const int64_t n2 = count / 2;
-  const int64_t per = 256LL * 4;  // elements (double2) per block at 4 per thread
+  const int64_t per = 256LL * 2;  // elements (double2) per block at 2 per thread
   int64_t blocks = (n2 + per - 1) / per;
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   if (blocks > cap) blocks = cap;
