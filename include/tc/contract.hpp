@@ -56,6 +56,10 @@ struct TensorAllocator {
 };
 void* tensor_storage_allocate(std::size_t bytes);
 void tensor_storage_free(void* p, std::size_t bytes);
+/// Page-locks a large Tensor storage block (the base of a block of `bytes`
+/// from tensor_storage_allocate) for the rest of its life; false for small
+/// blocks or when registration fails (transfers then take the pageable path).
+bool tensor_storage_pin(const void* p, std::size_t bytes);
 template <typename T>
 T* TensorAllocator<T>::allocate(std::size_t n) {
   return static_cast<T*>(tensor_storage_allocate(n * sizeof(T)));

@@ -233,6 +233,8 @@ DeviceRecipe lower_checked(const ValidatedContraction& v, bool* groups_ok,
 // to the output-label mode).
 // -1 if none; the widest rows win.
 constexpr std::int64_t kMinRow = 32 << 10;
+// streamed paths: the operand uploaded whole may be pageable up to this size
+constexpr std::int64_t kSmallPageable = 4 << 20;
 // output-label mode: streamed operand + output bytes per slab (TC_SLAB_MB overrides)
 std::int64_t slab_bytes() {
   static const std::int64_t b = [] {
@@ -645,7 +647,12 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
   tcb_host_is_pinned(left, &pinned_l);
   tcb_host_is_pinned(right, &pinned_r);
   tcb_host_is_pinned(out, &pinned_o);
-  if (label < 0 || slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
+  // the streamed operand and the output must be page-locked; the operand that
+  // goes up whole first may be pageable when small (tc::execute's operands:
+  // only large tensor blocks are pinned)
+  const bool other_ok = (on_left ? pinned_r : pinned_l) ||
+                        (on_left ? nr_ : nl_) * 8 <= kSmallPageable;
+  if (label < 0 || slabs < 2 || !((on_left ? pinned_l : pinned_r) && pinned_o && other_ok)) {
     upload(left, right);
     run();
     download(out);
@@ -852,7 +859,9 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
   tcb_host_is_pinned(left, &pinned_l);
   tcb_host_is_pinned(right, &pinned_r);
   tcb_host_is_pinned(out, &pinned_o);
-  if (slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
+  const bool other_ok = (on_left ? pinned_r : pinned_l) ||
+                        (on_left ? nr_ : nl_) * 8 <= kSmallPageable;
+  if (slabs < 2 || !((on_left ? pinned_l : pinned_r) && pinned_o && other_ok)) {
     upload(left, right);
     run();
     download(out);
@@ -1045,12 +1054,24 @@ std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
     dev->tick("execute");
     PreparedContraction pc(v, dev->options().device);
     mark("prepare");
-    pc.upload(left.data(), right.data());
-    mark("upload");
-    pc.run();
-    mark("run");
-    pc.download(out.data());
-    mark("download");
+    // large operands and result page-locked (once per storage block): the
+    // streamed path overlaps their transfers with the contraction
+    const auto bytes = [](const Tensor& t) { return static_cast<std::size_t>(t.size()) * 8; };
+    const bool pl = tensor_storage_pin(left.data(), bytes(left));
+    const bool pr = tensor_storage_pin(right.data(), bytes(right));
+    const bool po = tensor_storage_pin(out.data(), bytes(out));
+    mark("pin");
+    if (po && (pl || pr)) {  // run_streamed checks the rest (a small operand may stay pageable)
+      pc.run_streamed(left.data(), right.data(), out.data());
+      mark("streamed");
+    } else {
+      pc.upload(left.data(), right.data());
+      mark("upload");
+      pc.run();
+      mark("run");
+      pc.download(out.data());
+      mark("download");
+    }
     st.kernel_calls = pc.launches_last_run();
     st.packed_bytes = pc.permuted_bytes();
   } catch (const std::invalid_argument&) {
