@@ -141,3 +141,19 @@ def test_peer_ksplit_errors(dev):
     T.check(dev.tcb_peer_granularity(C.byref(g)))
     assert dev.tcb_peer_alloc(g.value + 8, C.byref(C.c_void_p()), C.byref(C.c_int())) == 1
     assert dev.tcb_peer_free(C.c_void_p(64)) == 1
+
+
+def test_peer_ksplit_level2_and_permuted_recipes(dev):
+    # GEMV-shaped partials (m or n = 1: the level-2 kernels write the scattered
+    # output through the same composite addressing) ...
+    _ksplit_virtual(dev, "R[+a] = T[+a,+b,+g] * G[-b,-g]", "a=96,b=12,g=10", "b", 3)
+    _ksplit_virtual(dev, "R[+a,+c] = T[+b,+a] * G[-b,+c]", "a=1,b=64,c=40", "b", 2)
+    # ... and a class-3.1 recipe whose operand is permuted before the GEMM
+    _ksplit_virtual(dev, "R[+b,-e] = A[+a,+b,+g] * B[-g,-a,-e]", "a=8,b=24,g=6,e=32", "a", 2)
+
+
+def test_peer_scatter_refuses_scalar_output(dev):
+    p = T.Prepared("K[] = T[+a,+b] * S[-a,-b]", "a=8,b=4")
+    with pytest.raises(ValueError, match="no label to split"):
+        p.run_scattered(0, 2, 1 << 20)
+    p.close()
