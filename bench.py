@@ -285,6 +285,11 @@ def main() -> int:
     cfg = args.config
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if os.environ.get("TCB_BENCH_EXTENTS"):  # plumbing tests only, never a BASELINE number
+        e, _, d = CONFIGS[cfg]
+        CONFIGS[cfg] = (e, os.environ["TCB_BENCH_EXTENTS"],
+                        d + " [extents overridden by TCB_BENCH_EXTENTS: plumbing test, not the "
+                            "BASELINE workload]")
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
 
@@ -336,7 +341,10 @@ def main() -> int:
         # then each rank sums its received slots (partition.PeerKSplit)
         block = info["output"] // world
         scat = T.DeviceBuffer(block * 8)
-        exchange = P.PeerKSplit(dev, world, rank, block, torch.distributed)
+        # ranks sharing one GPU (gloo plumbing runs): host barriers between the
+        # phases instead of device-side flag waits across processes
+        exchange = P.PeerKSplit(dev, world, rank, block, torch.distributed,
+                                host_sync=backend != "nccl")
 
         def collective():
             pass

@@ -201,11 +201,16 @@ class PeerKSplit:
     other; used by the GPU tests)."""
 
     def __init__(self, dev, world: int, rank: int | None, block: int, dist=None, group=None,
-                 _local: int = 1):
+                 _local: int = 1, host_sync: bool = False):
         import ctypes as C
         import os
         from . import native
         self.dev, self.world, self.rank, self.block = dev, world, rank, block
+        # host_sync: a host barrier between the scatter and the reduction, so
+        # no reduction kernel ever waits for another process's kernels (ranks
+        # sharing one GPU in plumbing tests); on one GPU per rank the reduction
+        # waits on the flags instead
+        self.dist, self.group, self.host_sync = dist, group, host_sync
         self.epoch = 0
         gran = C.c_int64()
         native.check(dev.tcb_peer_granularity(C.byref(gran)), "tcb_peer_granularity")
@@ -263,9 +268,16 @@ class PeerKSplit:
                                               self.epoch), "tcb_peer_reduce")
 
     def step(self, prep, out_ptr: int) -> None:
+        from . import native
         self.begin()
         self.scatter(prep)
+        if self.host_sync:
+            native.check(self.dev.tcb_sync(), "tcb_sync")
+            self.dist.barrier(group=self.group)
         self.reduce(out_ptr)
+        if self.host_sync:  # nobody scatters the next step into slots still being reduced
+            native.check(self.dev.tcb_sync(), "tcb_sync")
+            self.dist.barrier(group=self.group)
 
     def close(self) -> None:
         from . import native
