@@ -740,6 +740,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int in = 0; in < 4; ++in) dmma(acc[im][in], a[im], b[in]);
       }
+      // Release the stage only once every lane's fragment loads from it have
+      // completed: ptxas issues the arrive as soon as the loads are issued
+      // (their DMMAs may follow it), and the producer's next TMA write to the
+      // stage could then land before a late load reads it (seen as a corrupt
+      // warp tile when slow epilogues let the producer run ahead).
+      // fence.cta waits for this thread's outstanding loads.
+      asm volatile("fence.acq_rel.cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * stage);
       ++gcons;

@@ -37,6 +37,7 @@ namespace {
 struct Side {
   std::vector<int> modes;              // non-unit label ids in mode order
   std::vector<std::int64_t> stride;    // per label id (canonical), 0 if absent
+  std::vector<std::int64_t> extent;    // per label id: iteration extent
   std::int64_t elements = 1;
 };
 
@@ -45,6 +46,7 @@ struct Side {
 Side side_of(const ValidatedContraction& v, const ValidatedContraction& layout, bool right) {
   Side s;
   s.stride.assign(v.labels.size(), 0);
+  s.extent.assign(v.labels.size(), 1);
   const int rank = right ? v.right_rank() : v.left_rank();
   std::int64_t run = 1, elems = 1;
   for (int m = 0; m < rank; ++m) {
@@ -52,6 +54,7 @@ Side side_of(const ValidatedContraction& v, const ValidatedContraction& layout, 
     const LabelInfo& lo = right ? layout.label_at_right_mode(m) : layout.label_at_left_mode(m);
     const int id = v.label_index(li.label);
     s.stride[static_cast<std::size_t>(id)] = run;
+    s.extent[static_cast<std::size_t>(id)] = li.extent;
     run *= lo.extent;
     elems *= li.extent;
     if (li.extent > 1) s.modes.push_back(id);
@@ -60,16 +63,25 @@ Side side_of(const ValidatedContraction& v, const ValidatedContraction& layout, 
   return s;
 }
 
-// Maximal runs of consecutive (non-unit) modes whose labels satisfy `in`.
+// Maximal runs of consecutive (non-unit) modes whose labels satisfy `in` and
+// whose strides chain (stride[next] == stride[prev] * extent[prev]): always
+// true for a whole tensor; a slab of a label in the middle of a run (the
+// streamed paths lower slabs with the whole tensor's strides) breaks it there.
 template <typename Pred>
 std::vector<std::vector<int>> runs(const Side& s, Pred in) {
   std::vector<std::vector<int>> out;
   bool open = false;
+  int prev = -1;
   for (int id : s.modes) {
     if (in(id)) {
-      if (!open) out.emplace_back();
+      const bool chained =
+          open && s.stride[static_cast<std::size_t>(id)] ==
+                      s.stride[static_cast<std::size_t>(prev)] *
+                          s.extent[static_cast<std::size_t>(prev)];
+      if (!chained) out.emplace_back();
       out.back().push_back(id);
       open = true;
+      prev = id;
     } else {
       open = false;
     }

@@ -81,3 +81,34 @@ def test_stream_k_hybrid_and_pure_shapes_with_beta(dev, m, n, k, beta):
     ref = 0.75 * (A.reshape(k, m).T @ B.reshape(n, k).T) + beta * C0.reshape(n, m).T
     assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (m, n, k, beta)
     assert info.grid == 148 and info.splits >= 2, (info.grid, info.splits)
+
+
+@pytest.mark.parametrize("x", ["b=64,f=4096,g=48,e=64", "b=32,f=4096,g=48,e=64"])
+def test_short_k_with_scattered_output_is_race_free(dev, x):
+    """Regression: many short tiles (2-4 k-blocks) whose output rows are
+    scattered (no TMA store; the plain-store epilogue is slower than the main
+    loop), so the producer refills ring stages as soon as the consumers
+    release them. The release must wait for the consumers' fragment loads
+    (gemm_dmma.cu: fence before the empty-barrier arrive); without it a warp
+    tile was occasionally computed from a half-overwritten stage. Five runs
+    must agree bit for bit and match numpy (BLAS fp64) within 1e-12."""
+    e = "R[-g,+f,-e] = A[-b,+f,-g] * B[+b,-e]"
+    ext = dict((k, int(v)) for k, v in (kv.split("=") for kv in x.split(",")))
+    p = T.Prepared(e, x)
+    inf = p.info()
+    L, R = T.seeded(inf["left"], 1), T.seeded(inf["right"], 2)
+    want = np.einsum("gfb,eb->efg", L.reshape(ext["g"], ext["f"], ext["b"]),
+                     R.reshape(ext["e"], ext["b"])).reshape(-1)
+    first = None
+    for _ in range(5):
+        p.upload(L, R)
+        p.run()
+        out = np.empty(want.size)
+        p.download(out)
+        if first is None:
+            first = out
+            assert O.rel_frobenius(out, want) <= 1e-12
+            assert O.max_rel_error(out, want) <= 1e-12
+        else:
+            assert np.array_equal(out.view(np.uint64), first.view(np.uint64))
+    p.close()

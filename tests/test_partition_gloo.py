@@ -100,8 +100,8 @@ def _fd_worker(rank, world, port, q):
         os.close(fd)
         seen = []
         for f in fds:
-            os.lseek(f, 0, os.SEEK_SET)
-            seen.append(os.read(f, 64).decode())
+            # pread: a passed descriptor shares its file offset with the sender's
+            seen.append(os.pread(f, 64, 0).decode())
             os.close(f)
         q.put((rank, seen))
     finally:
