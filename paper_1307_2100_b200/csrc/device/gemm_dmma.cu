@@ -635,6 +635,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             *dst = use_beta ? fma(p.beta, *dst, v[j]) : v[j];
           }
         }
+        // the staging loads must have completed before the consumers may
+        // overwrite the buffer (see the ring-stage release in the main loop)
+        asm volatile("fence.acq_rel.cta;" ::: "memory");
         mbar_arrive(stg_empty);
       }
       return;
