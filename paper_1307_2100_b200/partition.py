@@ -212,9 +212,10 @@ class PeerKSplit:
         # waits on the flags instead
         self.dist, self.group, self.host_sync = dist, group, host_sync
         self.epoch = 0
+        self.slot = block + (block & 1)  # slots start 16-byte aligned
         gran = C.c_int64()
         native.check(dev.tcb_peer_granularity(C.byref(gran)), "tcb_peer_granularity")
-        slots = 2 * world * block * 8  # two parity sets of `world` slots
+        slots = 2 * world * self.slot * 8  # two parity sets of `world` slots
         self.flag_off = -(-slots // 256) * 256
         self.stride = -(-(self.flag_off + 8 * world) // gran.value) * gran.value
         self.own = []  # local allocations (1, or `world` in a virtual exchange)
@@ -244,7 +245,7 @@ class PeerKSplit:
         return cls(dev, world, None, block, _local=world)
 
     def _parity(self) -> int:
-        return (self.epoch % 2) * self.world * self.block * 8
+        return (self.epoch % 2) * self.world * self.slot * 8
 
     def begin(self) -> None:
         """Starts a step (all ranks' scatters of this step use its epoch)."""
@@ -254,7 +255,7 @@ class PeerKSplit:
         """Rank `rank`'s contraction, every block written into its owner's slot."""
         from . import native
         r = self.rank if rank is None else rank
-        base = self.window + self._parity() + r * self.block * 8
+        base = self.window + self._parity() + r * self.slot * 8
         prep.run_scattered(base, self.world, self.stride // 8)
         native.check(self.dev.tcb_peer_signal(self.window, self.stride, self.flag_off, r,
                                               self.world, self.epoch), "tcb_peer_signal")
@@ -264,7 +265,7 @@ class PeerKSplit:
         from . import native
         mine = self.own[0] if owner is None else self.own[owner]
         native.check(self.dev.tcb_peer_reduce(mine + self._parity(), self.world, self.block,
-                                              self.block, out_ptr, mine + self.flag_off,
+                                              self.slot, out_ptr, mine + self.flag_off,
                                               self.epoch), "tcb_peer_reduce")
 
     def step(self, prep, out_ptr: int) -> None:

@@ -117,6 +117,8 @@ def test_peer_ksplit_cfg5_shape(dev, world):
 def test_peer_ksplit_ragged_and_odd(dev):
     # odd extents (cp.async path, ragged tiles), block of odd element count
     _ksplit_virtual(dev, "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=37,j=6,k=5,l=6", "l", 3)
+    # odd block (37 x 3 elements per owner): slots padded to 16-byte alignment
+    _ksplit_virtual(dev, "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=37,j=6,k=5,l=6", "l", 2)
 
 
 def test_peer_ksplit_outermost_label_in_rows_and_batch(dev):
