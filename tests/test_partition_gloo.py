@@ -135,3 +135,83 @@ def test_slab_bounds_cover_exactly():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
     with pytest.raises(ValueError):
         P.shard_free("C[+i,+j] = A[+i,+k] * B[-k,+j]", "i=2,j=2,k=2", "k", 2, 0)
+
+
+class _FakeDev:
+    """Stands in for libtcb200 (no GPU here): records the peer calls so the
+    address arithmetic of PeerKSplit can be checked on the CPU."""
+
+    def __init__(self):
+        self.calls, self.next_ptr = [], 1 << 32
+
+    def tcb_peer_granularity(self, out):
+        out._obj.value = 2 << 20
+        return 0
+
+    def tcb_peer_alloc(self, nbytes, p, fd):
+        p._obj.value = self.next_ptr
+        self.next_ptr += 1 << 36
+        fd._obj.value = os.open(os.devnull, os.O_RDONLY)
+        self.calls.append(("alloc", nbytes))
+        return 0
+
+    def tcb_peer_window(self, n, fds, stride, w):
+        w._obj.value = 7 << 40
+        self.calls.append(("window", n, stride))
+        return 0
+
+    def tcb_peer_signal(self, win, stride, flag_off, rank, world, epoch):
+        self.calls.append(("signal", win, stride, flag_off, rank, world, epoch))
+        return 0
+
+    def tcb_peer_reduce(self, slots, world, count, slot_stride, out, flags, epoch):
+        self.calls.append(("reduce", slots, world, count, slot_stride, out, flags, epoch))
+        return 0
+
+    def tcb_peer_free(self, p):
+        self.calls.append(("free", p))
+        return 0
+
+
+class _FakePrep:
+    def __init__(self):
+        self.calls = []
+
+    def run_scattered(self, base, parts, part_stride):
+        self.calls.append((base, parts, part_stride))
+
+
+@pytest.mark.parametrize("world,block", [(1, 64), (3, 1000), (4, 111), (8, 8 * 1024 * 1024)])
+def test_peer_ksplit_layout_arithmetic(world, block):
+    """Host logic of the fused K-split exchange (partition.PeerKSplit): rank r
+    writes block o into owner o's slot r of the step's parity set, through the
+    window stride; owners reduce their own parity set; flags sit after both
+    sets; the allocation is a granularity multiple; odd blocks get even slots."""
+    dev, prep = _FakeDev(), _FakePrep()
+    ex = P.PeerKSplit.virtual(dev, world, block)
+    slot = block + (block & 1)
+    assert ex.slot == slot and ex.stride % (2 << 20) == 0
+    assert ex.flag_off >= 2 * world * slot * 8 and ex.flag_off + 8 * world <= ex.stride
+    win = 7 << 40
+    for step in (1, 2, 3):
+        ex.begin()
+        parity = (step % 2) * world * slot * 8
+        for r in range(world):
+            ex.scatter(prep, rank=r)
+            base, parts, part_stride = prep.calls[-1]
+            assert (base, parts, part_stride) == (win + parity + r * slot * 8, world,
+                                                  ex.stride // 8)
+            # block o of rank r lands in owner o's allocation, slot r
+            for o in range(world):
+                addr = base + o * part_stride * 8
+                assert (addr - win) // ex.stride == o
+                assert (addr - win) % ex.stride == parity + r * slot * 8
+            assert dev.calls[-1] == ("signal", win, ex.stride, ex.flag_off, r, world, step)
+        for o in range(world):
+            ex.reduce(1234, owner=o)
+            _, slots, w, count, ss, out, flags, epoch = dev.calls[-1]
+            assert (w, count, ss, out, epoch) == (world, block, slot, 1234, step)
+            assert slots == ex.own[o] + parity and flags == ex.own[o] + ex.flag_off
+            assert slots % 16 == 0
+    ex.close()
+    assert [c[0] for c in dev.calls[-(world + 1):]] == ["free"] * (world + 1)
