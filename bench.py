@@ -550,6 +550,10 @@ def main() -> int:
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if clk and clk.get("sm_max_mhz"):
+        # nominal DMMA peak at the maximum SM clock: SMs x 128 flop/clk
+        line["roofline"]["peak_nominal"] = round(
+            148 * 128 * float(clk["sm_max_mhz"]) * 1e6 / 1e12, 3)
     prof = ROOT / "profiles" / f"ncu_{cfg}_summary.json"
     if prof.exists():
         try:
