@@ -25,7 +25,7 @@ def num(d, key):
         x = float(v.replace(",", ""))
     except ValueError:
         return None
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6,
              "ms": 1e-3, "s": 1, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
              "Ghz": 1e9, "Mhz": 1e6, "hz": 1}.get(u, 1)
     return x * scale
