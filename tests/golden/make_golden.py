@@ -8,7 +8,7 @@ Run here (the reference does not exist on the GPU box):
   reports.json  ref_report text (classify/enumerate/plan/render/relayout)
   small.npz     tc::execute (reference backend, auto plan) and
                 tc::contract_naive results on small seeded contractions
-  baseline.json reference tc::execute results of BASELINE cfg1-cfg3 at full
+  baseline.json reference tc::execute results of BASELINE cfg1-cfg4 at full
                 size: checksums + 512 sampled entries
 """
 import json
@@ -82,9 +82,9 @@ def main():
     np.savez_compressed(HERE / "small.npz", **arrays)
     (HERE / "small.json").write_text(json.dumps(meta, indent=0))
 
-    # BASELINE cfg1-3 full size: checksums + samples of the reference result
+    # BASELINE cfg1-4 full size: checksums + samples of the reference result
     base = {}
-    for name in ("cfg1", "cfg2", "cfg3"):
+    for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
         e, x = BASELINE[name]
         res, st = O.ref_execute(e, x, seed=1, workers=8)
         idx = np.random.default_rng(7).choice(res.size, 512, replace=False)

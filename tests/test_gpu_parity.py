@@ -98,7 +98,7 @@ def test_results_are_bit_reproducible(dev):
     assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4"])
 def test_baseline_configs_full_size(dev, cfg):
     g = json.loads((GOLD / "baseline.json").read_text())[cfg]
     got, st = T.execute(g["expr"], g["extents"], seed=1)
@@ -109,6 +109,8 @@ def test_baseline_configs_full_size(dev, cfg):
     assert np.abs(got[idx] - val).max() / scale <= TOL
     assert abs(got.sum() - g["sum"]) <= 1e-9 * abs(g["sumsq"]) ** 0.5 * 10
     assert abs((got * got).sum() - g["sumsq"]) <= 1e-11 * g["sumsq"]
+    if cfg == "cfg4":  # 2.2 TFLOP on the CPU: the committed fixture is the reference
+        return
     live = O.ref_execute(g["expr"], g["extents"], seed=1, workers=16)
     if live is not None:
         assert close(got, live[0])
