@@ -91,6 +91,17 @@ def main():
         base[name] = {"expr": e, "extents": x, "n": int(res.size), "sum": float(res.sum()),
                       "sumsq": float((res * res).sum()), "idx": idx.tolist(),
                       "val": res[idx].tolist(), "flops": st["flops"]}
+    # cfg5: the reference result for the j < 64 column slab (j is B's and C's
+    # outermost label, so B's first 64 columns are the first values of its
+    # seeded stream and the slab contraction computes C[:, :64] exactly)
+    e, x = BASELINE["cfg5"]
+    xs = x.replace("j=8192", "j=64")
+    res, st = O.ref_execute(e, xs, seed=1, workers=8)
+    idx = np.random.default_rng(7).choice(res.size, 512, replace=False)
+    base["cfg5_slab"] = {"expr": e, "extents": x, "slab": "j<64", "slab_extents": xs,
+                         "n": int(res.size), "sum": float(res.sum()),
+                         "sumsq": float((res * res).sum()), "idx": idx.tolist(),
+                         "val": res[idx].tolist(), "flops": st["flops"]}
     (HERE / "baseline.json").write_text(json.dumps(base))
     print("golden fixtures written to", HERE)
 

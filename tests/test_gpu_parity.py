@@ -178,6 +178,15 @@ def test_cfg5_full_size_sampled(dev):
     p.download(got)
     assert np.isfinite(got).all() and del_ok
     assert _sampled_check(e, x, got, L, R, 40, np.random.default_rng(5)) <= TOL
+    # the compiled reference's result for the j < 64 column slab (committed
+    # fixture, tests/golden/make_golden.py): j is C's outermost label, so the
+    # slab is the first 8192 * 64 entries
+    g = json.loads((GOLD / "baseline.json").read_text())["cfg5_slab"]
+    slab = got[:g["n"]]
+    idx, val = np.array(g["idx"]), np.array(g["val"])
+    assert np.abs(slab[idx] - val).max() / max(1.0, np.abs(val).max()) <= TOL
+    assert abs((slab * slab).sum() - g["sumsq"]) <= 1e-11 * g["sumsq"]
+    assert abs(slab.sum() - g["sum"]) <= 1e-9 * g["sumsq"] ** 0.5 * 10
 
 
 @pytest.mark.parametrize("name,e,x", [
