@@ -53,3 +53,17 @@ def test_custom_experiment_and_errors(dev):
         T.bench_csv("square3d", sizes=(4,), repetitions=0)
     with pytest.raises(ValueError, match="size sweep must be nonempty"):
         T.bench_csv("square3d", sizes=())
+
+
+def test_execute_loop_with_pinned_recycled_blocks(dev):
+    """tc::execute in a loop on large tensors (tc::run_bench repetitions): the
+    operands are page-locked on the first call and every result lands in a
+    recycled pinned block, evaluated through the streamed pipeline; the
+    harness's sampled-line verification must pass on every configuration."""
+    for e, x in [("C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]", "a=256,b=256,c=64,k=256"),
+                 ("C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=512,j=512,k=64,l=64"),
+                 ("C[+a,+b,+i,+j] = A[+a,+b,+k,+l] * B[-k,-l,+i,+j]",
+                  "a=256,b=64,i=32,j=32,k=32,l=32")]:
+        text, ok = T.bench_csv("custom", sizes=(1,), kernels=("GEMM",), repetitions=4,
+                               verify=True, custom_expr=e, custom_extents=x)
+        assert ok, (e, x, text)
