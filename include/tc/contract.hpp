@@ -357,6 +357,14 @@ std::unique_ptr<KernelBackend> make_b200_backend(const B200Options& options = {}
 /// engine: they throw std::invalid_argument naming the replacement.
 std::unique_ptr<KernelBackend> make_backend(const std::string& name);
 
+/// The reference's CPU factories (include/tc/kernels.hpp:41-45), declared so
+/// that callers written against the reference compile and link unchanged.
+/// This engine has no CPU contraction path: both throw std::invalid_argument
+/// naming make_b200_backend(). A caller's own KernelBackend subclass still
+/// works with execute() (driven slice by slice, like the reference).
+std::unique_ptr<KernelBackend> make_reference_backend();
+std::unique_ptr<KernelBackend> make_eigen_backend();
+
 // ============================================================ L4: executor
 // reference: include/tc/executor.hpp:14-54
 
@@ -368,14 +376,36 @@ struct ExecutionStats {
   double wall_seconds = 0.0;      // host wall time incl. transfers
 };
 
-/// Runs the contraction on the device: the plan is checked against the
-/// operands (extent drift), lowered to one device recipe (permutations +
-/// one GEMM/GEMV/DOT launch) and executed. `workers` is accepted for source
-/// compatibility; results are bit-identical for any value.
+/// Runs the contraction. The plan is checked against the operands (extent
+/// drift). With the B200 backend it is lowered to one device recipe
+/// (permutations + one GEMM/GEMV/DOT launch) and executed; `workers` does not
+/// change the result (bit-identical for any value). With any other
+/// KernelBackend the plan's loop nest is walked and the backend called once
+/// per slice, free slices spread over `workers` threads — the reference's
+/// behaviour (src/executor.cpp:102-369), kept for callers that plug in their
+/// own backend (fault injection, instrumentation, a host BLAS).
 std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
                                           const ValidatedContraction& v, const Tensor& left,
                                           const Tensor& right, const KernelBackend& backend,
                                           int workers = 1);
+
+/// execute() on caller-owned storage (no reference counterpart; the C-ABI's
+/// tcf_execute_host): `left`/`right` hold the operands in generalized
+/// column-major order of v's operand shapes, `out` receives the whole result
+/// (output order of v). With the B200 backend, page-locked buffers
+/// (tcb_host_register / tcb_host_alloc) take the streamed path (uploads,
+/// contraction and download overlapped); pageable ones go through the
+/// staging buffers.
+ExecutionStats execute_into(const ExecutionPlan& plan, const ValidatedContraction& v,
+                            const double* left, const double* right, double* out,
+                            const KernelBackend& backend, int workers = 1);
+
+/// The loop-over-kernel driver behind execute() for non-B200 backends: one
+/// backend call per slice of the plan's loop nest (stats accumulated into
+/// `stats`). `out` must be zero-filled on entry.
+void execute_sliced(const ExecutionPlan& plan, const ValidatedContraction& v, const double* left,
+                    const double* right, double* out, const KernelBackend& backend, int workers,
+                    ExecutionStats& stats);
 
 struct SlicingRun {
   SlicingVector s_left, s_right;

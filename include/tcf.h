@@ -32,6 +32,19 @@ int tcf_execute(const char* expr, int positional, const char* extents, uint64_t 
                 double* out, int64_t out_cap, int64_t* stats, double* seconds, char* err,
                 int64_t errcap);
 
+/* tc::execute (include/tc/executor.hpp:28-32 of the reference) on CALLER
+ * host buffers: parse -> validate -> plan -> execute with the b200 backend.
+ * `left`/`right` hold the operands in generalized column-major order of the
+ * expression's operand shapes, `out` (out_cap doubles) receives the whole
+ * result. Page-locked buffers (tcb_host_register / tcb_host_alloc) take the
+ * streamed path (H2D, DMMA and D2H overlapped); pageable buffers go through
+ * pinned staging. policy/kernel/s_left/s_right/stats/seconds as tcf_execute.
+ * This is the drop-in call bench.py's e2e number is measured through. */
+int tcf_execute_host(const char* expr, int positional, const char* extents, const double* left,
+                     const double* right, double* out, int64_t out_cap, int workers, int policy,
+                     int kernel, const char* s_left, const char* s_right, int64_t* stats,
+                     double* seconds, char* err, int64_t errcap);
+
 /* The device recipe (lowering) of a contraction, without touching a device:
  * "L1|L2|L3 gemm m=.. n=.. k=.. a(sm,sk) b(sk,sn) batch=[..] permutes=N", or
  * "L4 gemm m=.. n=.. k=.. m[ext:str,..] n[..] k[ext:str_a/str_b,..] ..." for

@@ -190,6 +190,67 @@ __attribute__((visibility("default"))) int ref_execute(
   }
 }
 
+// Bound contraction for repeated timing (bench.py's reference arm): operands
+// seeded and the plan built once by ref_bind; ref_run is one tc::execute
+// (src/executor.cpp:287-369) with the reference backend, its wall time in
+// *seconds (ExecutionStats::wall_seconds); `out` may be null.
+struct RefBound {
+  Bound b;
+  tc::ExecutionPlan plan;
+};
+
+__attribute__((visibility("default"))) void* ref_bind(const char* expr, int positional,
+                                                      const char* extents, std::uint64_t seed,
+                                                      int policy, int kernel, const char* sl,
+                                                      const char* sr, char* err,
+                                                      std::int64_t errcap) {
+  try {
+    auto* h = new RefBound{bind(expr, positional, extents, seed), {}};
+    tc::PlanPolicy pol;
+    if (policy == 1) pol = tc::PlanPolicy::force_kernel(static_cast<tc::KernelKind>(kernel));
+    if (policy == 2) pol = tc::PlanPolicy::force_slicing(parse_vec(sl), parse_vec(sr));
+    try {
+      h->plan = tc::plan(h->b.v, pol);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    return h;
+  } catch (const std::exception& e) {
+    fail(e, err, errcap, 1);
+    return nullptr;
+  }
+}
+
+__attribute__((visibility("default"))) int ref_run(void* handle, int workers, double* out,
+                                                   std::int64_t out_cap, std::int64_t* stats,
+                                                   double* seconds, char* err,
+                                                   std::int64_t errcap) {
+  try {
+    auto* h = static_cast<RefBound*>(handle);
+    const auto backend = tc::make_reference_backend();
+    auto [res, st] = tc::execute(h->plan, h->b.v, h->b.left, h->b.right, *backend, workers);
+    if (out) {
+      if (res.size() > out_cap) throw std::invalid_argument("output buffer too small");
+      std::memcpy(out, res.data(), static_cast<std::size_t>(res.size()) * 8);
+    }
+    if (stats) {
+      stats[0] = st.kernel_calls;
+      stats[1] = st.packed_bytes;
+      stats[2] = st.staged_bytes;
+      stats[3] = st.flops;
+    }
+    if (seconds) *seconds = st.wall_seconds;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, err, errcap, 1);
+  }
+}
+
+__attribute__((visibility("default"))) void ref_release(void* handle) {
+  delete static_cast<RefBound*>(handle);
+}
+
 __attribute__((visibility("default"))) int ref_naive(const char* expr, int positional,
                                                      const char* extents, std::uint64_t seed,
                                                      std::int64_t work_cap, double* out,

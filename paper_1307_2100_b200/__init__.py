@@ -20,7 +20,7 @@ from .native import GemmDesc, GemmInfo, TcbError, check
 
 KERNELS = ["GEMM", "COPY+GEMM", "GEMV", "COPY+GEMV", "GER", "DOT", "ELEMENTWISE"]
 
-__all__ = ["report", "lower", "execute", "seeded", "Prepared", "DeviceBuffer", "GemmDesc", "GemmInfo",
+__all__ = ["report", "lower", "execute", "execute_host", "seeded", "Prepared", "DeviceBuffer", "GemmDesc", "GemmInfo",
            "TcbError", "check", "native", "KERNELS", "parse_expr"]
 
 
@@ -85,6 +85,31 @@ def execute(expr: str, extents: str, seed: int = 1, positional: bool = False, wo
     _err(rc, err)
     return out, {"kernel_calls": stats[0], "packed_bytes": stats[1], "staged_bytes": stats[2],
                  "flops": stats[3], "wall_seconds": secs.value}
+
+
+def execute_host(expr: str, extents: str, left: np.ndarray, right: np.ndarray,
+                 out: np.ndarray, positional: bool = False, workers: int = 1,
+                 kernel: str | None = None, slicing: tuple[str, str] | None = None) -> dict:
+    """tc::execute on caller host buffers (tcf_execute_host): `out` receives
+    the result; page-locked buffers take the streamed path. Returns stats."""
+    for a in (left, right, out):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise ValueError("execute_host needs contiguous float64 arrays")
+    stats = (C.c_int64 * 4)()
+    secs = C.c_double()
+    err = C.create_string_buffer(4096)
+    policy, kidx, sl, sr = 0, 0, b"", b""
+    if kernel is not None:
+        policy, kidx = 1, KERNELS.index(kernel.upper())
+    if slicing is not None:
+        policy, sl, sr = 2, slicing[0].encode(), slicing[1].encode()
+    rc = native.front().tcf_execute_host(expr.encode(), int(positional), extents.encode(),
+                                         left.ctypes.data, right.ctypes.data, out.ctypes.data,
+                                         out.size, workers, policy, kidx, sl, sr, stats,
+                                         C.byref(secs), err, len(err))
+    _err(rc, err)
+    return {"kernel_calls": stats[0], "packed_bytes": stats[1], "staged_bytes": stats[2],
+            "flops": stats[3], "wall_seconds": secs.value}
 
 
 def tensor_text(extents, variance: str, seed: int, name: str = "t") -> str:

@@ -179,6 +179,36 @@ int tcf_execute(const char* expr, int positional, const char* extents, uint64_t 
   TCF_GUARD(err, errcap)
 }
 
+int tcf_execute_host(const char* expr, int positional, const char* extents, const double* left,
+                     const double* right, double* out, int64_t out_cap, int workers, int policy,
+                     int kernel, const char* s_left, const char* s_right, int64_t* stats,
+                     double* seconds, char* err, int64_t errcap) {
+  try {
+    const tc::ContractionSpec spec = tc::parse(expr ? expr : "", positional != 0);
+    const Shapes s = shapes_of(spec, parse_extents(extents));
+    const tc::ValidatedContraction v = tc::validate_shapes(spec, s.le, s.lv, s.re, s.rv);
+    std::int64_t n = 1;
+    for (std::int64_t e : v.output_extents()) n *= e;
+    if (n > out_cap) throw std::invalid_argument("output buffer too small");
+    if (!left || !right || !out) throw std::invalid_argument("null operand or result buffer");
+    tc::PlanPolicy pol;
+    if (policy == 1) pol = tc::PlanPolicy::force_kernel(static_cast<tc::KernelKind>(kernel));
+    if (policy == 2) pol = tc::PlanPolicy::force_slicing(vec_parse(s_left), vec_parse(s_right));
+    const tc::ExecutionPlan p = tc::plan(v, pol);
+    static const auto backend = tc::make_b200_backend();
+    const tc::ExecutionStats st = tc::execute_into(p, v, left, right, out, *backend, workers);
+    if (stats) {
+      stats[0] = st.kernel_calls;
+      stats[1] = st.packed_bytes;
+      stats[2] = st.staged_bytes;
+      stats[3] = st.flops;
+    }
+    if (seconds) *seconds = st.wall_seconds;
+    return 0;
+  }
+  TCF_GUARD(err, errcap)
+}
+
 int tcf_lower(const char* expr, int positional, const char* extents, char* buf, int64_t cap) {
   try {
     const tc::ContractionSpec spec = tc::parse(expr ? expr : "", positional != 0);

@@ -144,6 +144,18 @@ std::unique_ptr<KernelBackend> make_b200_backend(const B200Options& options) {
   return std::make_unique<B200Backend>(options);
 }
 
+std::unique_ptr<KernelBackend> make_reference_backend() {
+  throw std::invalid_argument(
+      "make_reference_backend: the reference's CPU backend is not part of this engine, which "
+      "runs on the B200: use make_b200_backend()");
+}
+
+std::unique_ptr<KernelBackend> make_eigen_backend() {
+  throw std::invalid_argument(
+      "make_eigen_backend: the Eigen CPU backend is not part of this engine, which runs on the "
+      "B200: use make_b200_backend()");
+}
+
 std::unique_ptr<KernelBackend> make_backend(const std::string& name) {
   if (name == "b200" || name == "device") return make_b200_backend();
   if (name == "reference" || name == "external")
@@ -1013,30 +1025,25 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
 
 // ------------------------------------------------------------------ execute
 
-std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
-                                          const ValidatedContraction& v, const Tensor& left,
-                                          const Tensor& right, const KernelBackend& backend,
-                                          int workers) {
-  (void)workers;  // one device launch; the result does not depend on it
-  // plan/operand consistency (reference: src/executor.cpp:292-303)
+namespace {
+
+// plan / contraction consistency (reference: src/executor.cpp:292-297); the
+// operand extents are checked by the Tensor overload
+void check_plan(const ExecutionPlan& plan, const ValidatedContraction& v) {
   if (plan.label_extents.size() != v.labels.size())
     throw std::invalid_argument("plan does not match contraction");
-  for (std::size_t i = 0; i < v.labels.size(); ++i) {
-    const LabelInfo& li = v.labels[i];
-    if (li.extent != plan.label_extents[i])
+  for (std::size_t i = 0; i < v.labels.size(); ++i)
+    if (v.labels[i].extent != plan.label_extents[i])
       throw std::invalid_argument("extent drift between planning and execution on label '" +
-                                  li.label + "'");
-    if (li.left_mode >= 0 && left.extent(li.left_mode) != li.extent)
-      throw std::invalid_argument("left operand extent drift on label '" + li.label + "'");
-    if (li.right_mode >= 0 && right.extent(li.right_mode) != li.extent)
-      throw std::invalid_argument("right operand extent drift on label '" + li.label + "'");
-  }
-  const auto* dev = dynamic_cast<const B200Backend*>(&backend);
-  if (!dev)
-    throw std::invalid_argument("execute: backend '" + backend.name() +
-                                "' has no device path; use tc::make_backend(\"b200\")");
+                                  v.labels[i].label + "'");
+}
 
-  const auto t0 = std::chrono::steady_clock::now();
+// One contraction on the device over host storage: lowered once, then either
+// the streamed pipeline (H2D / DMMA / D2H overlapped; needs page-locked
+// storage) or upload + run + download.
+void run_on_device(const B200Backend& dev, const ValidatedContraction& v, const double* left,
+                   const double* right, double* out, bool streamed, ExecutionStats& st,
+                   const std::chrono::steady_clock::time_point& t0) {
   // TC_EXEC_TRACE=1: phase times of this call on stderr (diagnostics)
   static const bool trace = std::getenv("TC_EXEC_TRACE") != nullptr;
   auto mark = [&](const char* what) {
@@ -1045,31 +1052,19 @@ std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
                                                              t0).count());
   };
-  Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name,
-             Tensor::Uninit{});  // overwritten whole by the download
-  mark("output");
-  ExecutionStats st;
-  st.flops = plan.flops;
   try {
-    dev->tick("execute");
-    PreparedContraction pc(v, dev->options().device);
+    dev.tick("execute");
+    PreparedContraction pc(v, dev.options().device);
     mark("prepare");
-    // large operands and result page-locked (once per storage block): the
-    // streamed path overlaps their transfers with the contraction
-    const auto bytes = [](const Tensor& t) { return static_cast<std::size_t>(t.size()) * 8; };
-    const bool pl = tensor_storage_pin(left.data(), bytes(left));
-    const bool pr = tensor_storage_pin(right.data(), bytes(right));
-    const bool po = tensor_storage_pin(out.data(), bytes(out));
-    mark("pin");
-    if (po && (pl || pr)) {  // run_streamed checks the rest (a small operand may stay pageable)
-      pc.run_streamed(left.data(), right.data(), out.data());
+    if (streamed) {
+      pc.run_streamed(left, right, out);
       mark("streamed");
     } else {
-      pc.upload(left.data(), right.data());
+      pc.upload(left, right);
       mark("upload");
       pc.run();
       mark("run");
-      pc.download(out.data());
+      pc.download(out);
       mark("download");
     }
     st.kernel_calls = pc.launches_last_run();
@@ -1080,6 +1075,74 @@ std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
     throw std::runtime_error(std::string(e.what()) + " while executing " +
                              lower(v).summary() + " for " + unparse(v.spec));
   }
+}
+
+bool host_pinned(const void* p) {
+  int pinned = 0;
+  return p && tcb_host_is_pinned(p, &pinned) == TCB_OK && pinned;
+}
+
+}  // namespace
+
+ExecutionStats execute_into(const ExecutionPlan& plan, const ValidatedContraction& v,
+                            const double* left, const double* right, double* out,
+                            const KernelBackend& backend, int workers) {
+  check_plan(plan, v);
+  const auto t0 = std::chrono::steady_clock::now();
+  ExecutionStats st;
+  st.flops = plan.flops;
+  if (const auto* dev = dynamic_cast<const B200Backend*>(&backend)) {
+    // caller-owned storage is never registered here: it streams when the
+    // caller page-locked it (tcb_host_register / tcb_host_alloc)
+    static const bool off = std::getenv("TC_NO_PIN") != nullptr;
+    const bool streamed =
+        !off && host_pinned(out) && (host_pinned(left) || host_pinned(right));
+    run_on_device(*dev, v, left, right, out, streamed, st, t0);
+  } else {
+    std::int64_t n = 1;
+    for (std::int64_t e : v.output_extents()) n *= e;
+    std::fill(out, out + n, 0.0);
+    execute_sliced(plan, v, left, right, out, backend, workers, st);
+  }
+  st.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return st;
+}
+
+std::pair<Tensor, ExecutionStats> execute(const ExecutionPlan& plan,
+                                          const ValidatedContraction& v, const Tensor& left,
+                                          const Tensor& right, const KernelBackend& backend,
+                                          int workers) {
+  // plan/operand consistency (reference: src/executor.cpp:292-303)
+  check_plan(plan, v);
+  for (const LabelInfo& li : v.labels) {
+    if (li.left_mode >= 0 && left.extent(li.left_mode) != li.extent)
+      throw std::invalid_argument("left operand extent drift on label '" + li.label + "'");
+    if (li.right_mode >= 0 && right.extent(li.right_mode) != li.extent)
+      throw std::invalid_argument("right operand extent drift on label '" + li.label + "'");
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  ExecutionStats st;
+  st.flops = plan.flops;
+  const auto* dev = dynamic_cast<const B200Backend*>(&backend);
+  if (!dev) {
+    // any other KernelBackend: the reference's loop over kernel calls
+    Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name);
+    execute_sliced(plan, v, left.data(), right.data(), out.data(), backend, workers, st);
+    st.wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return {std::move(out), st};
+  }
+  Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name,
+             Tensor::Uninit{});  // overwritten whole by the download
+  // large operands and result page-locked (once per storage block): the
+  // streamed path overlaps their transfers with the contraction
+  const auto bytes = [](const Tensor& t) { return static_cast<std::size_t>(t.size()) * 8; };
+  const bool pl = tensor_storage_pin(left.data(), bytes(left));
+  const bool pr = tensor_storage_pin(right.data(), bytes(right));
+  const bool po = tensor_storage_pin(out.data(), bytes(out));
+  // run_streamed checks the rest (a small operand may stay pageable)
+  run_on_device(*dev, v, left.data(), right.data(), out.data(), po && (pl || pr), st, t0);
   st.wall_seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return {std::move(out), st};

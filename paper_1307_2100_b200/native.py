@@ -112,6 +112,8 @@ TCF_API = {
     "tcf_report": (i32, [cp, i32, cp, cp, i64]),
     "tcf_execute": (i32, [cp, i32, cp, C.c_uint64, i32, i32, i32, cp, cp, vp, i64, P_i64,
                           P_f64, cp, i64]),
+    "tcf_execute_host": (i32, [cp, i32, cp, vp, vp, vp, i64, i32, i32, i32, cp, cp, P_i64,
+                               P_f64, cp, i64]),
     "tcf_lower": (i32, [cp, i32, cp, cp, i64]),
     "tcf_seeded": (i32, [i64, C.c_uint64, vp]),
     "tcf_prepare": (i32, [cp, i32, cp, i32, C.POINTER(vp), cp, i64]),

@@ -1,6 +1,7 @@
 // Host-front suites restated from the reference's doctest files
 // (tests/test_tensor.cpp, test_expr.cpp, test_planner.cpp) against the
 // engine's tc:: API. CPU only.
+#include <cstring>
 #include <set>
 
 #include "harness.hpp"
@@ -200,6 +201,186 @@ TEST_CASE("only the device backend exists") {
   CHECK(make_backend("b200")->name() == "b200");
   CHECK_THROWS_AS(make_backend("reference"), std::invalid_argument);
   CHECK_THROWS_AS(make_backend("nope"), std::invalid_argument);
+  // the reference's factories link, and name the replacement
+  CHECK_THROWS_AS(make_reference_backend(), std::invalid_argument);
+  CHECK_THROWS_AS(make_eigen_backend(), std::invalid_argument);
+}
+
+// ------------------------------------------- caller-supplied KernelBackend
+// execute() drives any non-B200 backend slice by slice, as the reference does
+// (src/executor.cpp:102-369). A plain host BLAS written here (test code).
+namespace {
+class HostBlas : public KernelBackend {
+ public:
+  mutable std::int64_t calls = 0;
+  const std::string& name() const override {
+    static const std::string n = "host-test";
+    return n;
+  }
+  bool supports_transpose() const override { return true; }
+  void gemm(bool ta, bool tb, std::int64_t m, std::int64_t n, std::int64_t k, double alpha,
+            const double* a, std::int64_t lda, const double* b, std::int64_t ldb, double beta,
+            double* c, std::int64_t ldc) const override {
+    ++calls;
+    for (std::int64_t j = 0; j < n; ++j)
+      for (std::int64_t i = 0; i < m; ++i) {
+        double s = 0;
+        for (std::int64_t p = 0; p < k; ++p)
+          s += (ta ? a[p + i * lda] : a[i + p * lda]) * (tb ? b[j + p * ldb] : b[p + j * ldb]);
+        c[i + j * ldc] = alpha * s + (beta == 0 ? 0.0 : beta * c[i + j * ldc]);
+      }
+  }
+  void gemv(bool trans, std::int64_t m, std::int64_t n, double alpha, const double* a,
+            std::int64_t lda, const double* x, std::int64_t incx, double beta, double* y,
+            std::int64_t incy) const override {
+    ++calls;
+    const std::int64_t rows = trans ? n : m, inner = trans ? m : n;
+    for (std::int64_t r = 0; r < rows; ++r) {
+      double s = 0;
+      for (std::int64_t q = 0; q < inner; ++q)
+        s += (trans ? a[q + r * lda] : a[r + q * lda]) * x[q * incx];
+      y[r * incy] = alpha * s + (beta == 0 ? 0.0 : beta * y[r * incy]);
+    }
+  }
+  void ger(std::int64_t m, std::int64_t n, double alpha, const double* x, std::int64_t incx,
+           const double* y, std::int64_t incy, double* a, std::int64_t lda) const override {
+    ++calls;
+    for (std::int64_t j = 0; j < n; ++j)
+      for (std::int64_t i = 0; i < m; ++i) a[i + j * lda] += alpha * x[i * incx] * y[j * incy];
+  }
+  double dot(std::int64_t k, const double* x, std::int64_t incx, const double* y,
+             std::int64_t incy) const override {
+    ++calls;
+    double s = 0;
+    for (std::int64_t i = 0; i < k; ++i) s += x[i * incx] * y[i * incy];
+    return s;
+  }
+};
+
+class FailingBlas : public HostBlas {
+ public:
+  explicit FailingBlas(int after) : after_(after) {}
+  void gemm(bool ta, bool tb, std::int64_t m, std::int64_t n, std::int64_t k, double alpha,
+            const double* a, std::int64_t lda, const double* b, std::int64_t ldb, double beta,
+            double* c, std::int64_t ldc) const override {
+    if (calls >= after_) throw std::runtime_error("injected backend failure");
+    HostBlas::gemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+  }
+
+ private:
+  int after_;
+};
+
+// brute force over every label (test code)
+std::vector<double> brute(const tst::Bound& b) {
+  const auto& v = b.v;
+  std::vector<double> out(static_cast<std::size_t>(
+      [&] { std::int64_t n = 1; for (auto e : v.output_extents()) n *= e; return n; }()), 0.0);
+  const std::size_t nl = v.labels.size();
+  std::vector<std::int64_t> at(nl, 0);
+  for (;;) {
+    std::int64_t lo = 0, ro = 0, oo = 0;
+    for (std::size_t i = 0; i < nl; ++i) {
+      const auto& li = v.labels[i];
+      if (li.left_mode >= 0) lo += at[i] * stride_of(b.left, li.left_mode);
+      if (li.right_mode >= 0) ro += at[i] * stride_of(b.right, li.right_mode);
+      if (li.output_mode >= 0) {
+        std::int64_t s = 1;
+        for (int m = 0; m < li.output_mode; ++m) s *= v.output_extents()[static_cast<std::size_t>(m)];
+        oo += at[i] * s;
+      }
+    }
+    out[static_cast<std::size_t>(oo)] += b.left.data()[lo] * b.right.data()[ro];
+    std::size_t k = 0;
+    for (; k < nl; ++k) {
+      if (++at[k] < v.labels[k].extent) break;
+      at[k] = 0;
+    }
+    if (k == nl) break;
+  }
+  return out;
+}
+
+double max_rel(const Tensor& got, const std::vector<double>& want) {
+  double scale = 1, worst = 0;
+  for (double w : want) scale = std::max(scale, std::fabs(w));
+  for (std::size_t i = 0; i < want.size(); ++i)
+    worst = std::max(worst, std::fabs(got.data()[i] - want[i]));
+  return worst / scale;
+}
+}  // namespace
+
+TEST_CASE("a caller's backend runs every slicing slice by slice") {  // test_executor.cpp:89-102
+  const char* exprs[] = {
+      "C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]",
+      "C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]",
+      "C[+a,+b,+c,+d] = A[+a,+k,+c,+l] * B[-l,+b,-k,+d]",
+      "R[+a,-e] = A[+a,+b,+g] * B[-e,-b,-g]",
+      "R[+a] = T[+a,+b,+g] * G[-b,-g]",
+      "K[] = T[+a,+b,+g] * S[-a,-b,-g]",
+      "C[+b,+a] = A[+k,+a] * B[-k,+b]",
+  };
+  const std::map<std::string, std::int64_t> ext{{"i", 5}, {"j", 4}, {"k", 3}, {"l", 2},
+                                               {"a", 4}, {"b", 3}, {"c", 2}, {"d", 3},
+                                               {"e", 2}, {"g", 3}};
+  HostBlas be;
+  for (const char* e : exprs) {
+    const auto b = bind_expr(e, ext);
+    const auto want = brute(b);
+    for (const auto& o : enumerate_slicings(b.v)) {
+      ExecutionPlan p;
+      try {
+        p = plan(b.v, PlanPolicy::force_slicing(o.s_left, o.s_right));
+      } catch (const kernel_unreachable_error&) {
+        continue;
+      }
+      be.calls = 0;
+      const auto [res, st] = execute(p, b.v, b.left, b.right, be);
+      CHECK(max_rel(res, want) <= 1e-13);
+      CHECK(st.flops == p.flops);
+      CHECK(st.kernel_calls >= 1);
+      if (p.kernel != KernelKind::Elementwise) CHECK(st.kernel_calls == be.calls);
+      std::int64_t nest = 1;
+      for (const auto& l : p.loop_nest) nest *= l.extent;
+      if (p.kernel != KernelKind::Dot || p.kernel_map.k2_label < 0) CHECK(st.kernel_calls == nest);
+      const bool copies = p.kernel == KernelKind::CopyGemm || p.kernel == KernelKind::CopyGemv;
+      if (!copies) CHECK(st.packed_bytes == 0);
+      // workers do not change the result (include/tc/executor.hpp:25-27)
+      const auto [res4, st4] = execute(p, b.v, b.left, b.right, be, 4);
+      CHECK(std::memcmp(res.data(), res4.data(), static_cast<std::size_t>(res.size()) * 8) == 0);
+      CHECK(st4.kernel_calls == st.kernel_calls);
+    }
+  }
+}
+
+TEST_CASE("a failing backend's error carries the slice coordinates") {  // test_executor.cpp:240-291
+  const auto b = bind_expr("C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]",
+                           {{"i", 4}, {"j", 4}, {"k", 3}, {"l", 5}});
+  const ExecutionPlan p = plan(b.v);  // class 3.2: GEMM per l slice
+  FailingBlas be(2);
+  try {
+    execute(p, b.v, b.left, b.right, be);
+    CHECK(false);
+  } catch (const std::runtime_error& e) {
+    CHECK(std::string(e.what()) == "injected backend failure at slice coordinates [l=2]");
+  }
+  // the same through a worker pool: the first error propagates
+  FailingBlas be2(0);
+  CHECK_THROWS_AS(execute(p, b.v, b.left, b.right, be2, 3), std::runtime_error);
+}
+
+TEST_CASE("execute_into with a caller's backend fills caller storage") {
+  const auto b = bind_expr("C[+a,+b,+c] = A[+a,+k,+c] * B[-k,+b]",
+                           {{"a", 3}, {"b", 4}, {"c", 2}, {"k", 5}});
+  HostBlas be;
+  const ExecutionPlan p = plan(b.v);
+  std::vector<double> out(24, 7.0);  // overwritten whole
+  const ExecutionStats st = execute_into(p, b.v, b.left.data(), b.right.data(), out.data(), be);
+  const auto want = brute(b);
+  double worst = 0;
+  for (std::size_t i = 0; i < want.size(); ++i) worst = std::max(worst, std::fabs(out[i] - want[i]));
+  CHECK(worst <= 1e-13);
+  CHECK(st.kernel_calls == 2);  // one GEMM per c slice
 }
 
 TH_MAIN

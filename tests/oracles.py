@@ -45,13 +45,16 @@ def tco() -> C.CDLL:
     return _cache["tco"]
 
 
-def ref():
-    if "ref" not in _cache:
-        so = ORACLE / "_ref" / "libtcref.so"
+def ref(variant: str = ""):
+    """The compiled reference; variant "" (-O3 -DNDEBUG, the reference's own
+    flags), "_v3" (-march=x86-64-v3) or "_v4" (-march=x86-64-v4)."""
+    key = "ref" + variant
+    if key not in _cache:
+        so = ORACLE / "_ref" / f"libtcref{variant}.so"
         if not so.exists() and Path("/root/reference/proj/src").is_dir():
             subprocess.run(["make", "-C", str(ORACLE), "ref"], check=True, capture_output=True)
         if not so.exists():
-            _cache["ref"] = None
+            _cache[key] = None
             return None
         lib = C.CDLL(str(so))
         lib.ref_report.argtypes = [cp, C.c_int, cp, cp, i64]
@@ -63,8 +66,68 @@ def ref():
                                  i64, cp, i64]
         lib.ref_tensor_text.argtypes = [P_i64, C.c_int, cp, C.c_uint64, cp, cp, i64]
         lib.ref_read_tensor_text.argtypes = [cp, vp, i64, P_i64, cp, i64]
-        _cache["ref"] = lib
-    return _cache["ref"]
+        lib.ref_bind.argtypes = [cp, C.c_int, cp, C.c_uint64, C.c_int, C.c_int, cp, cp, cp, i64]
+        lib.ref_bind.restype = vp
+        lib.ref_run.argtypes = [vp, C.c_int, vp, i64, P_i64, C.POINTER(f64), cp, i64]
+        lib.ref_release.argtypes = [vp]
+        lib.ref_release.restype = None
+        _cache[key] = lib
+    return _cache[key]
+
+
+def native_variant() -> str:
+    """The highest -march level of the compiled reference this host's CPU runs:
+    "_v4" with AVX-512 (F, BW, CD, DQ, VL), "_v3" with AVX2 + FMA + BMI2, else ""."""
+    try:
+        flags = set()
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                flags = set(line.split(":", 1)[1].split())
+                break
+    except OSError:
+        return ""
+    if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl", "avx2", "fma", "bmi2"} <= flags:
+        return "_v4"
+    if {"avx2", "fma", "bmi2", "movbe"} <= flags:
+        return "_v3"
+    return ""
+
+
+class RefBound:
+    """A contraction bound once in the compiled reference (seeded operands,
+    auto plan); run() is one tc::execute with the reference backend and
+    returns its wall seconds (ExecutionStats::wall_seconds)."""
+
+    def __init__(self, expr: str, extents: str, seed: int = 1, variant: str = "",
+                 positional: bool = False):
+        self.lib = ref(variant)
+        if self.lib is None:
+            raise RuntimeError(f"oracle/_ref/libtcref{variant}.so missing")
+        err = C.create_string_buffer(4096)
+        self.h = self.lib.ref_bind(expr.encode(), int(positional), extents.encode(), seed, 0, 0,
+                                   b"", b"", err, len(err))
+        if not self.h:
+            raise RuntimeError(f"reference bind failed: {err.value.decode()}")
+
+    def run(self, workers: int = 1, out: np.ndarray | None = None) -> float:
+        secs = C.c_double()
+        err = C.create_string_buffer(4096)
+        rc = self.lib.ref_run(self.h, workers, None if out is None else out.ctypes.data,
+                              0 if out is None else out.size, None, C.byref(secs), err, len(err))
+        if rc != 0:
+            raise RuntimeError(f"reference run failed: {err.value.decode()}")
+        return secs.value
+
+    def close(self):
+        if self.h:
+            self.lib.ref_release(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- helpers
