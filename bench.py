@@ -4,36 +4,45 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config cfg1..cfg5]
 
-A *step* is one evaluation of the BASELINE contraction (default cfg2 =
-BASELINE.json configs[1]: C[a,b,c] = sum_k A[a,k,c] B[k,b], a=b=c=k=256, the
-class-2 shape the reference loops GEMM over; here one strided-batched DMMA
-launch). Prints ONE JSON line on rank 0.
+Default workload: BASELINE.json configs[4] (cfg5), the largest config that
+fits one GPU: C[i,j] = sum_{k,l} A[i,k,l] B[k,l,j], i=j=8192, k=l=512
+(35.2 TFLOP per step, 34.9 GB of operands + result). A *step* is one
+evaluation of the contraction. Prints ONE JSON line on rank 0.
 
-  value    GFLOP/s, operands resident in HBM, CUDA-event timed over exactly K
-           steps, max over ranks; flops = plan.flops = 2*prod(extents).
-           Consecutive steps use programmatic dependent launch (the next
-           contraction's prologue and main loop overlap the previous one's
-           tail; TCB_NO_PDL=1 disables it). Working sets that fit in L2
-           (cfg1) rotate over independent operand copies (>= 2 x L2 in all)
-           so no step re-reads hot data (--l2 flush: flush L2 before every
-           step instead, each step timed alone).
-  e2e      the same metric through the public plan-level API with pinned HOST
-           buffers, every step's H2D of its inputs and D2H of its result inside
-           the timed region: tcf_run_streamed_async (slabs overlapping H2D /
-           DMMA / D2H, successive steps pipelined, tcf_sync at the end); the
-           K-split (cfg5, N>1) uses upload + the fused scatter/reduce (or, with
-           --exchange nccl, run + tcb_reduce_scatter) + D2H of the rank's block.
-  roofline the DMMA GEMM kernel alone (CUDA events on its own stream) against
-           the fp64 DMMA peak measured live on this GPU (tcb_fp64_peak);
-           traffic = DRAM bytes per launch from profiles/ncu_<cfg>_summary.json.
-  cpu_baseline the unmodified reference (oracle/_ref, compiled from
-           /root/reference) on the host cores, rank 0, N=1 only.
+  value    GFLOP/s of the whole job: plan.flops of the FULL contraction x K /
+           (CUDA-event time of exactly K steps, max over ranks); operands
+           resident in HBM; flops = 2*prod(extents) (src/expr.cpp:257-261).
+           Consecutive steps use programmatic dependent launch.
+  e2e      the same metric through the drop-in call tc::execute on caller host
+           buffers (tcf_execute_host, include/tcf.h): every step parses, plans,
+           uploads its operands from pinned host memory, contracts and
+           downloads its result inside the timed region. The repo's pipelined
+           API (tcf_run_streamed_async) is reported beside it as
+           e2e.pipelined. For the K-split at N>1: upload + fused scatter/reduce
+           + D2H of the rank's block.
+  roofline the DMMA GEMM launch alone (CUDA events on its own stream) against
+           the fp64 DMMA peak measured live on this GPU (tcb_fp64_peak; the
+           driver's MEASURED_PEAKS.json has no fp64 entry); traffic = DRAM
+           bytes per launch from profiles/ncu_<cfg>_summary.json.
+  parity   the step's result checked against the committed golden samples of
+           the reference (tests/golden/baseline.json) on every rank's own
+           output block; parity_ok = all ranks within 1e-12.
+  cpu_baseline  the unmodified reference (oracle/_ref, compiled from
+           /root/reference) timed on the host cores on a bounded sample of the
+           same workload (rank 0, N=1), at workers=nproc and workers=1 and with
+           the -march build for this CPU.
+
+Multi-GPU (--gpus N; the driver launches torchrun, or bench.py spawns it):
+  cfg5   contracted l split N ways, partial C reduce-scattered along j — fused
+         into the GEMM epilogue over peer memory (default) or NCCL
+         (--exchange nccl); strong scaling
+  cfg1-4 a free label split N ways (cfg1 j, cfg2 c, cfg3 d, cfg4 b), no
+         data-path collective; strong scaling
+Each rank generates only its own slabs of the seeded operands (tcf_seeded_block).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref)
-on all host cores for the same config and prints the same line with
-"impl": "reference". Under torchrun (N>1) every rank runs its own c-slab of
-a weakly scaled problem (no collective on the data path); only rank 0 runs
-the reference arm.
+on all host cores on a bounded sample of the same workload per step and
+prints the same line with "impl": "reference" (rank 0 only under torchrun).
 """
 from __future__ import annotations
 
@@ -44,6 +53,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 import weakref
 from pathlib import Path
@@ -66,17 +76,37 @@ CONFIGS = {
              "a=256,b=256,i=64,j=64,k=64,l=64",
              "BASELINE configs[3]: CCD C[a,b,i,j]=A[a,b,k,l]B[k,l,i,j], a=b=256, i..l=64"),
     "cfg5": ("C[+i,+j] = A[+i,+k,+l] * B[-k,-l,+j]", "i=8192,j=8192,k=512,l=512",
-             "BASELINE configs[4]: large class-1, i=j=8192, k=l=512"),
+             "BASELINE configs[4]: large class-1 C[i,j]=A[i,k,l]B[k,l,j], i=j=8192, k=l=512 "
+             "(largest BASELINE config that fits one GPU: 34.9 GB)"),
 }
-# How a config runs on N ranks (BASELINE.json / SURVEY.md §8e):
-#   weak   each rank evaluates its own full-size slab of a free label (no collective)
-#   shard  strong scaling: the free label is split across ranks (no collective; cfg4 splits b)
-#   ksplit strong scaling: the contracted label is split, partial C reduce-scattered along
-#          the outermost output label (cfg5: split l, scatter j): by default fused into
-#          the GEMM epilogue over peer memory (--exchange peer), or NCCL after the GEMM
-MODE = {"cfg1": ("weak", "j"), "cfg2": ("weak", "c"), "cfg3": ("weak", "d"),
+# How a config runs on N > 1 ranks. Every mode is strong
+# scaling: the full BASELINE contraction is split across the ranks.
+#   shard  a free label split N ways, no data-path collective
+#   ksplit the contracted label split N ways, partial C reduce-scattered along
+#          the outermost output label (cfg5: split l, scatter j)
+MODE = {"cfg1": ("shard", "j"), "cfg2": ("shard", "c"), "cfg3": ("shard", "d"),
         "cfg4": ("shard", "b"), "cfg5": ("ksplit", "l")}
+# Bounded CPU samples of each workload for the reference arm and cpu_baseline
+# (a full cfg5 on the reference is ~1.2 h on one core, cfg4 ~40 s): extents of
+# a sub-contraction whose per-call kernel shape equals the full plan's. The
+# reference's GEMM packs 256-column panels of B (kernels_reference.cpp:50-53),
+# so a 256-column j-slab runs exactly one panel per call, as every panel of
+# the full call does; 8 of the 512 l-iterations of its loop nest.
+CPU_SAMPLE = {
+    "cfg1": ("i=512,j=512,k=64,l=64", "the full cfg1 contraction"),
+    "cfg2": ("a=256,b=256,c=256,k=256", "the full cfg2 contraction"),
+    "cfg3": ("a=64,b=64,c=64,d=64,k=32,l=32", "the full cfg3 contraction"),
+    "cfg4": ("a=256,b=16,i=64,j=64,k=64,l=64",
+             "b<16 slab of cfg4 (1/16 of the work; the plan's per-call GEMM 256x64x64 and "
+             "loop nest b:free j:free l:contracted unchanged), scaled by flops"),
+    "cfg5": ("i=8192,j=256,k=512,l=8",
+             "j<256, l<8 slab of cfg5 (1/256 of the work): 8 of the 512 l-iterations of the "
+             "reference's loop nest, each the full 8192-row GEMM over one 256-column B panel "
+             "(the reference kernel's own panel width, so per-panel work equals the full "
+             "call's), scaled by flops — extrapolated"),
+}
 L2_BYTES = 126 * 2**20
+GOLDEN = ROOT / "tests" / "golden" / "baseline.json"
 
 
 def dist_env():
@@ -199,67 +229,126 @@ def pinned_array(n: int, dev) -> np.ndarray:
         weakref.finalize(a, dev.tcb_host_unregister, a.ctypes.data)
     return a
 
-
-def shard_extents(cfg: str, world: int, rank: int) -> str:
-    """Per-rank extents of the contraction this rank evaluates."""
-    from paper_1307_2100_b200 import partition as P
-    mode, label = MODE[cfg]
-    expr, extents, _ = CONFIGS[cfg]
-    if mode == "weak" or world == 1:
-        return extents
-    if mode == "shard":
-        return P.shard_free(expr, extents, label, world, rank).extents
-    return P.shard_contracted(expr, extents, label, world, rank).extents
+def ext_map(extents: str) -> dict:
+    return {k: int(v) for k, v in (kv.split("=") for kv in extents.split(",") if kv)}
 
 
-def cpu_reference(expr: str, extents: str, reps: int, workers: int):
-    """Times the unmodified reference CPU path (tc::execute, reference backend)
-    via oracle/_ref; falls back to our C port of the naive oracle on a slab."""
+def flops_of(extents: str) -> int:
+    return 2 * int(np.prod(list(ext_map(extents).values()), dtype=np.int64))
+
+
+def free_space(expr: str, extents: str) -> int:
+    """Free-slice count of the reference's auto plan (src/executor.cpp:330-336):
+    the reference's worker threads split only the free loops, so this bounds
+    the cores it can use."""
+    import paper_1307_2100_b200 as T
+    auto = T.report(expr, extents).split("auto:\n")[1]
+    nest = auto.split("loop_nest:")[1].split("\n")[0].split()
+    exts = [int(x) for x in auto.split("loop_extents:")[1].split("\n")[0].split()]
+    n = 1
+    for item, e in zip(nest, exts):
+        if item.endswith(":free"):
+            n *= e
+    return n
+
+
+def cpu_info() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def time_reference(expr: str, extents: str, workers: int, variant: str, reps: int,
+                   warmup: int = 1) -> list[float]:
+    """Wall seconds of `reps` tc::execute calls of the unmodified reference
+    (oracle/_ref) with the reference backend — TEST INFRASTRUCTURE, CPU arm only."""
     sys.path.insert(0, str(ROOT / "tests"))
-    import oracles  # TEST INFRASTRUCTURE: CPU baseline only
-    if oracles.ref() is not None:
-        times = []
-        oracles.ref_execute(expr, extents, seed=1, workers=workers)  # warm-up
-        for _ in range(reps):
-            _, st = oracles.ref_execute(expr, extents, seed=1, workers=workers)
-            times.append(st["wall_seconds"])
-        return statistics.median(times), "reference", workers
-    return None, "unavailable", 0
+    import oracles  # the CPU baseline only; never on the device path
+    b = oracles.RefBound(expr, extents, seed=1, variant=variant)
+    try:
+        for _ in range(warmup):
+            b.run(workers)
+        return [b.run(workers) for _ in range(reps)]
+    finally:
+        b.close()
 
 
-def run_reference_arm(args, cfg):
+def cpu_baseline(cfg: str) -> dict | None:
+    """The reference on the host cores, on CPU_SAMPLE[cfg]: workers = nproc
+    (the reported value), workers = 1, and the -march build for this CPU."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles
+    if oracles.ref() is None:
+        return None
+    expr = CONFIGS[cfg][0]
+    sample, what = CPU_SAMPLE[cfg]
+    nproc = os.cpu_count() or 1
+    fs = free_space(expr, sample)
+    fl = flops_of(sample)
+    native = oracles.native_variant()
+    runs = []
+    for variant, workers, flags in (("", nproc, "-O3 -DNDEBUG (reference CMake flags)"),
+                                    ("", 1, "-O3 -DNDEBUG (reference CMake flags)"),
+                                    (native, nproc, {"_v4": "-O3 -DNDEBUG -march=x86-64-v4",
+                                                     "_v3": "-O3 -DNDEBUG -march=x86-64-v3",
+                                                     "": "-O3 -DNDEBUG"}[native]
+                                     + " (-march=native equivalent for this CPU)")):
+        if oracles.ref(variant) is None:
+            continue
+        secs = statistics.median(time_reference(expr, sample, workers, variant, reps=3))
+        runs.append({"flags": flags, "workers": workers, "cores_used": min(workers, fs),
+                     "value": round(fl / secs / 1e9, 3), "unit": "GFLOP/s",
+                     "sample_s": round(secs, 4)})
+    head = runs[0]
+    return {"value": head["value"], "unit": "GFLOP/s", "cores": head["cores_used"],
+            "kind": "reference",
+            "sample": f"{what}; tc::execute with the reference backend, workers={nproc}, "
+                      f"median of 3 after 1 warm-up",
+            "extrapolated": cfg in ("cfg4", "cfg5"),
+            "host": f"{nproc} threads, {cpu_info()}",
+            "cores_note": ("the reference parallelises only free loops of its plan "
+                           f"(src/executor.cpp:330-336); this plan has {fs} free slice(s)"),
+            "variants": runs}
+
+
+def run_reference_arm(args, cfg) -> int:
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    expr, extents, desc = CONFIGS[cfg]
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles
     if oracles.ref() is None:
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libtcref.so missing (build with make -C oracle)"}))
         return 0
-    workers = os.cpu_count() or 1
-    ext = {k: int(v) for k, v in (kv.split("=") for kv in extents.split(","))}
-    flops = 2 * int(np.prod(list(ext.values())))
-    for _ in range(args.warmup):
-        oracles.ref_execute(expr, extents, seed=1, workers=workers)
-    secs = []
-    for _ in range(args.steps):
-        _, st = oracles.ref_execute(expr, extents, seed=1, workers=workers)
-        secs.append(st["wall_seconds"])
+    expr, extents, desc = CONFIGS[cfg]
+    sample, what = CPU_SAMPLE[cfg]
+    nproc = os.cpu_count() or 1
+    fs = free_space(expr, sample)
+    fl = flops_of(sample)
+    secs = time_reference(expr, sample, nproc, "", reps=args.steps, warmup=args.warmup)
     total = sum(secs)
-    value = flops * args.steps / total / 1e9
+    value = fl * args.steps / total / 1e9
+    full_s = flops_of(extents) / (value * 1e9)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: Tensor::seeded_random uniform[-1,1], seeds 1 (A) / 2 (B)",
         "config": {"workload": desc, "expr": expr, "extents": extents,
+                   "sample_extents": sample,
                    "path": "reference tc::execute + ReferenceBackend (oracle/_ref, -O3 -DNDEBUG)"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": workers,
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": min(nproc, fs),
                          "kind": "reference",
-                         "sample": f"full {cfg} contraction per step, workers={workers}"},
+                         "sample": f"{what}; one sample per step, workers={nproc}",
+                         "extrapolated": cfg in ("cfg4", "cfg5"),
+                         "extrapolated_full_step_s": round(full_s, 3),
+                         "host": f"{nproc} threads, {cpu_info()}"},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -267,13 +356,104 @@ def run_reference_arm(args, cfg):
     return 0
 
 
+def golden_parity(cfg: str, expr: str, full: str, label: str | None, lo: int, hi: int,
+                  got: np.ndarray) -> dict:
+    """Checks this rank's output block against the committed golden samples of
+    the reference's result (tests/golden/baseline.json, made from the compiled
+    reference by tests/golden/make_golden.py). `got` is the output slab
+    [lo, hi) along `label` (the whole output when label is None)."""
+    gold = json.loads(GOLDEN.read_text())
+    g = gold["cfg5_slab"] if cfg == "cfg5" else gold[cfg]
+    out = expr.split("=")[0]
+    out = [x.strip()[1:] for x in out[out.index("[") + 1:out.index("]")].split(",")]
+    em = ext_map(full)
+    idx = np.array(g["idx"], dtype=np.int64)
+    val = np.array(g["val"])
+    coords, rem = {}, idx.copy()
+    for x in out:
+        coords[x] = rem % em[x]
+        rem //= em[x]
+    sub = dict(em)
+    keep = np.ones(idx.size, bool)
+    if label is not None:
+        keep = (coords[label] >= lo) & (coords[label] < hi)
+        sub[label] = hi - lo
+    local = np.zeros(idx.size, np.int64)
+    run = 1
+    for x in out:
+        c = coords[x] - (lo if x == label else 0)
+        local += c * run
+        run *= sub[x]
+    res = {"samples": int(keep.sum()), "source": "tests/golden/baseline.json"
+           + (" (cfg5: the reference's j<64 column slab)" if cfg == "cfg5" else "")}
+    if keep.any():
+        want = val[keep]
+        err = float(np.abs(got[local[keep]] - want).max() / max(1.0, np.abs(val).max()))
+        res["max_rel_error"] = err
+        res["ok"] = bool(err <= 1e-12)
+    else:
+        res["ok"] = True
+    if label is None or (lo == 0 and hi == em[label]):
+        part = got[:g["n"]] if cfg == "cfg5" else got  # the slab is C's first n entries
+        ss = float((part * part).sum())
+        res["sumsq_rel"] = abs(ss - g["sumsq"]) / g["sumsq"]
+        res["ok"] = res["ok"] and res["sumsq_rel"] <= 1e-11
+    return res
+
+
+def relaunch(args) -> int:
+    """--gpus N without torchrun: spawn N ranks on this node."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def fill_operands(expr: str, full: str, label: str | None, lo: int, hi: int, L, R) -> None:
+    """This rank's slabs of the seeded operands (A: seed 1, B: seed 2), written
+    into L and R; the two streams are drawn concurrently."""
+    import paper_1307_2100_b200 as T
+    from paper_1307_2100_b200 import partition as P
+    _, left, right = P.parse(expr)
+    em = ext_map(full)
+    front = T.native.front()
+    errs = []
+
+    def gen(labels, seed, arr):
+        try:
+            ext = [em[x] for x in labels]
+            if label is None or label not in labels:
+                front.tcf_seeded(arr.size, seed, arr.ctypes.data)
+            else:
+                a = (C.c_int64 * len(ext))(*ext)
+                rc = front.tcf_seeded_block(seed, len(ext), a, labels.index(label), lo, hi,
+                                            arr.ctypes.data)
+                if rc:
+                    raise RuntimeError(front.tcf_last_error().decode())
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=gen, args=(left, 1, L)),
+          threading.Thread(target=gen, args=(right, 2, R))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="K-split (cfg5, N>1): partial-C blocks written into their owners' "
@@ -290,15 +470,21 @@ def main() -> int:
         CONFIGS[cfg] = (e, os.environ["TCB_BENCH_EXTENTS"],
                         d + " [extents overridden by TCB_BENCH_EXTENTS: plumbing test, not the "
                             "BASELINE workload]")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
 
-    rank, world, local = dist_env()
     # one GPU per rank; ranks beyond the visible GPUs share them round-robin
-    # (only used for single-GPU plumbing tests with TCB_DIST_BACKEND=gloo)
+    # (only for single-GPU plumbing tests with TCB_DIST_BACKEND=gloo)
     import paper_1307_2100_b200 as T
+    from paper_1307_2100_b200 import partition as P
+    dev = T.native.device()
     ndev = C.c_int(0)
-    T.native.device().tcb_device_count(C.byref(ndev))
+    dev.tcb_device_count(C.byref(ndev))
     local = local % max(1, ndev.value)
     torch = None
     backend = os.environ.get("TCB_DIST_BACKEND", "nccl")  # gloo: plumbing tests on one GPU
@@ -311,31 +497,40 @@ def main() -> int:
         else:
             dist.init_process_group(backend)
 
-    def max_over_ranks(x: float) -> float:
+    def all_reduce(x: float, op: str) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(t, op=getattr(torch.distributed.ReduceOp, op))
         return float(t.item())
 
-    import paper_1307_2100_b200 as T
-    from paper_1307_2100_b200 import partition as P
-    dev = T.native.device()
     T.check(dev.tcb_init(local), "tcb_init")
-    expr, full_extents, desc = CONFIGS[cfg]
+    expr, full, desc = CONFIGS[cfg]
     mode, label = MODE[cfg]
-    extents = shard_extents(cfg, world, rank)
+    if world == 1:
+        mode, label, lo, hi, extents = "single", None, 0, 0, full
+    else:
+        sh = (P.shard_free if mode == "shard" else P.shard_contracted)(expr, full, label,
+                                                                      world, rank)
+        lo, hi, extents = sh.lo, sh.hi, sh.extents
     peak = C.c_double()
     T.check(dev.tcb_fp64_peak(C.byref(peak)), "tcb_fp64_peak")
 
     prep = T.Prepared(expr, extents, device=local)
     info = prep.info()
-    flops = info["flops"]  # this rank's share
-    total_flops = flops * world if mode == "weak" else 2 * int(
-        np.prod([int(v.split("=")[1]) for v in full_extents.split(",")]))
-    collective = None
-    exchange = None
-    if mode == "ksplit" and world > 1 and args.exchange == "peer":
+    flops = info["flops"]           # this rank's share
+    total_flops = flops_of(full)    # the whole job (strong scaling)
+    L = pinned_array(info["left"], dev)
+    R = pinned_array(info["right"], dev)
+    O = pinned_array(info["output"], dev)
+    t_gen = time.time()
+    fill_operands(expr, full, label, lo, hi, L, R)
+    t_gen = time.time() - t_gen
+
+    collective = exchange = None
+    block = info["output"]
+    if mode == "ksplit" and args.exchange == "peer":
         # fused: the GEMM epilogue writes each block of this rank's partial C
         # into its owner's receive buffer through the peer window (tcb_peer_*),
         # then each rank sums its received slots (partition.PeerKSplit)
@@ -345,15 +540,15 @@ def main() -> int:
         # phases instead of device-side flag waits across processes
         exchange = P.PeerKSplit(dev, world, rank, block, torch.distributed,
                                 host_sync=backend != "nccl")
-
-        def collective():
-            pass
-    elif mode == "ksplit" and world > 1:
+    elif mode == "ksplit":
         if backend != "nccl":
             raise SystemExit("ksplit (cfg5) with --exchange nccl needs the nccl backend")
-        # the engine's own NCCL communicator (tcb_comm_*, include/tcb.h): rank 0's
-        # unique id goes to the others over the process group; the reduce-scatter
-        # runs on the engine's stream right behind the contraction
+        # the engine's own NCCL communicator (tcb_comm_*, include/tcb.h); the
+        # reduce-scatter runs on the engine's stream right behind the
+        # contraction. NCCL's algorithm and protocol are pinned so the summation
+        # order (and so the result) is the same run to run.
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         uid = (C.c_char * 128)()
         if rank == 0:
             T.check(dev.tcb_comm_unique_id(uid), "tcb_comm_unique_id")
@@ -368,11 +563,6 @@ def main() -> int:
 
         def collective():
             T.check(dev.tcb_reduce_scatter(optr, scat.ptr, block, comm), "tcb_reduce_scatter")
-    L = pinned_array(info["left"], dev)
-    R = pinned_array(info["right"], dev)
-    O = pinned_array(info["output"], dev)
-    T.native.front().tcf_seeded(L.size, 1 + 2 * rank, L.ctypes.data)
-    T.native.front().tcf_seeded(R.size, 2 + 2 * rank, R.ctypes.data)
     prep.upload(L, R)
 
     def barrier():
@@ -387,15 +577,14 @@ def main() -> int:
     # operands and output, together >= 2 x L2), so every step reads its
     # operands from HBM and the steps still run back to back; --l2 flush
     # instead writes a 2 x L2 buffer before every step, outside the timed
-    # region, and brackets each step by its own events (this also charges
-    # each step the GPU launch latency of a lone kernel, ~3.5 us).
+    # region, and brackets each step by its own events.
     ws_bytes = (info["left"] + info["right"] + info["output"]) * 8
     small = ws_bytes <= L2_BYTES
     flush = small and args.l2 == "flush"
     flush_buf = T.DeviceBuffer(2 * L2_BYTES) if flush else None
     preps = [prep]
     if small and not flush:
-        if collective is not None:
+        if mode == "ksplit":
             raise SystemExit("rotation with a collective is not supported")
         n_copies = -(-2 * L2_BYTES // ws_bytes)
         for _ in range(n_copies - 1):
@@ -448,9 +637,26 @@ def main() -> int:
     launches = dev.tcb_launch_count()
     clk = clocks.stop()
     barrier()
-    t_ms = max_over_ranks(total_ms)
+    t_ms = all_reduce(total_ms, "MAX")
     step_ms = t_ms / args.steps
     value = total_flops / (step_ms * 1e-3) / 1e9
+
+    # ---- parity of the timed steps' result: this rank's output block
+    barrier()
+    got = np.empty(block)
+    if mode == "ksplit":
+        T.check(dev.tcb_d2h(got.ctypes.data, scat.ptr, block * 8), "tcb_d2h")
+        # rank r owns the r-th block of the outermost output label (j)
+        out_last = expr.split("=")[0].split(",")[-1].strip(" ]+-")
+        n_out = ext_map(full)[out_last]
+        plo, phi, plabel = n_out * rank // world, n_out * (rank + 1) // world, out_last
+    else:
+        prep.download(got)
+        plo, phi, plabel = lo, hi, label
+    parity = golden_parity(cfg, expr, full, plabel, plo, phi, got)
+    parity["ranks_ok"] = all_reduce(1.0 if parity["ok"] else 0.0, "MIN") == 1.0
+    parity["samples_all_ranks"] = int(all_reduce(float(parity["samples"]), "SUM"))
+    del got
 
     # ---- the dominant kernel alone (the contraction launch), same L2 treatment
     n_kern = max(3, min(args.steps, 50, int(2000.0 / max(step_ms, 1e-3))))
@@ -462,61 +668,91 @@ def main() -> int:
     gemm_info = T.GemmInfo()
     dev.tcb_last_gemm_info(C.byref(gemm_info))
 
-    # ---- end to end through the public API with pinned host buffers
-    n_e2e = max(3, min(args.steps, 20, int(1000.0 / max(step_ms, 1e-3))))
-    slabs_used = 1
-    prep.upload(L, R)
-    prep.run()
-    prep.download(O)
-    if collective is None:
-        # untimed warm-up of the streamed path (its streams, events and second
-        # device buffer set are created on first use)
-        for _ in range(2):
-            prep.run_streamed(L, R, O, slabs=0, wait=False)
-        prep.sync()
+    # ---- end to end with host buffers
+    n_e2e = max(3, min(args.steps, 20, int(1500.0 / max(step_ms, 1e-3))))
     barrier()
-    # three timed rounds; the median round is reported (host-side PCIe / page
-    # effects make single short rounds noisy), all rounds are listed
-    rounds = []
-    for _ in range(3):
+    e2e = {"unit": "GFLOP/s", "h2d_bytes_per_step": int((info["left"] + info["right"]) * 8),
+           "d2h_bytes_per_step": int(block * 8), "steps": n_e2e}
+    if mode != "ksplit":
+        # (1) the drop-in call: tc::execute on the caller's pinned host buffers
+        # (tcf_execute_host), one synchronous call per step, result on the host
+        T.execute_host(expr, extents, L, R, O)  # warm-up (pool, streams)
+        rounds = []
+        for _ in range(3):
+            barrier()
+            T.check(dev.tcb_timer_start())
+            for _ in range(n_e2e):
+                T.execute_host(expr, extents, L, R, O)
+            T.check(dev.tcb_timer_stop(C.byref(ms)))
+            rounds.append(all_reduce(float(ms.value), "MAX") / n_e2e)
+        e2e_ms = statistics.median(rounds)
+        e2e.update({"value": round(total_flops / (e2e_ms * 1e-3) / 1e9, 3),
+                    "ms_per_step": round(e2e_ms, 4),
+                    "rounds_ms_per_step": [round(r, 4) for r in rounds],
+                    "api": "tc::execute on caller host buffers (tcf_execute_host, include/tcf.h; "
+                           "reference include/tc/executor.hpp:28-32): parse, plan, H2D from "
+                           "pinned memory overlapped with the DMMA contraction, D2H of the "
+                           "result, one synchronous call per step"})
+        e2e_check = golden_parity(cfg, expr, full, label, lo, hi, O)
+        e2e["parity_ok"] = bool(all_reduce(1.0 if e2e_check["ok"] else 0.0, "MIN") == 1.0)
+        # (2) the repo's pipelined API: successive steps overlap (two buffer sets)
+        slabs_used = 1
+        for _ in range(2):
+            slabs_used = prep.run_streamed(L, R, O, slabs=0, wait=False)
+        prep.sync()
         barrier()
         T.check(dev.tcb_timer_start())
         for _ in range(n_e2e):
-            if collective is not None:
+            prep.run_streamed(L, R, O, slabs=0, wait=False)
+        prep.sync()
+        T.check(dev.tcb_timer_stop(C.byref(ms)))
+        pipe_ms = all_reduce(float(ms.value), "MAX") / n_e2e
+        e2e["pipelined"] = {
+            "value": round(total_flops / (pipe_ms * 1e-3) / 1e9, 3),
+            "ms_per_step": round(pipe_ms, 4),
+            "api": "tcf_run_streamed_async: H2D / DMMA / D2H overlapped over %d slabs, "
+                   "successive steps pipelined over two device buffer sets, tcf_sync at the "
+                   "end" % slabs_used}
+    else:
+        rounds = []
+        out_view = np.empty(block)
+        for _ in range(3):
+            barrier()
+            T.check(dev.tcb_timer_start())
+            for _ in range(n_e2e):
                 prep.upload(L, R)
                 step()
-                out_view = np.empty(block)
-                T.check(dev.tcb_d2h(out_view.ctypes.data, scat.ptr, block * 8))
-            else:
-                # the public streamed host path: H2D of slab s+1, the contraction of
-                # slab s and the D2H of slab s-1 overlap (pinned buffers); successive
-                # steps are pipelined (step s+1's uploads overlap step s's last
-                # downloads), every step still moves its inputs up and its result down
-                slabs_used = prep.run_streamed(L, R, O, slabs=0, wait=False)
-        if collective is None:
-            prep.sync()  # the last step's result is on the host
-        T.check(dev.tcb_timer_stop(C.byref(ms)))
-        rounds.append(max_over_ranks(float(ms.value)) / n_e2e)
-    e2e_step_ms = statistics.median(rounds)
-    e2e_value = total_flops / (e2e_step_ms * 1e-3) / 1e9
+                T.check(dev.tcb_d2h(out_view.ctypes.data, scat.ptr, block * 8), "tcb_d2h")
+            T.check(dev.tcb_timer_stop(C.byref(ms)))
+            rounds.append(all_reduce(float(ms.value), "MAX") / n_e2e)
+        e2e_ms = statistics.median(rounds)
+        e2e.update({"value": round(total_flops / (e2e_ms * 1e-3) / 1e9, 3),
+                    "ms_per_step": round(e2e_ms, 4),
+                    "rounds_ms_per_step": [round(r, 4) for r in rounds],
+                    "api": ("tcf_upload + tcf_run_scattered into the peer window + "
+                            "tcb_peer_reduce + D2H of the rank's block" if exchange is not None
+                            else "tcf_upload + tcf_run + tcb_reduce_scatter (NCCL) + D2H of "
+                                 "the rank's block")})
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 6),
-        "higher_is_better": True, "scaling": "weak" if mode == "weak" else "strong",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: Tensor::seeded_random uniform[-1,1] (mt19937_64), seeds 1/2 (+2*rank)",
+        "data": "synthetic: Tensor::seeded_random uniform[-1,1] (mt19937_64), A seed 1, B seed 2 "
+                "(each rank draws its own slab of the same full tensors)",
         "config": {
-            "workload": desc, "expr": expr, "extents": extents,
+            "workload": desc, "expr": expr, "extents": full,
             "recipe": info["summary"],
             "parallelism": "single GPU" if world == 1 else {
-                "weak": f"weak: rank r owns its own full-size {label}-slab (no data-path collective)",
-                "shard": f"strong: {label} split {world} ways (no data-path collective)",
+                "shard": f"strong: free label {label} split {world} ways (rank {rank}: "
+                         f"{label} in [{lo},{hi})), no data-path collective",
                 "ksplit": f"strong: contracted {label} split {world} ways; partial C "
                           f"reduce-scattered over the outermost output label "
                           + ("fused: GEMM epilogue writes each block into its owner's receive "
                              "buffer over NVLink (tcb_peer_*), owner sums the slots"
-                             if exchange is not None else "by NCCL after the GEMM")}[mode],
+                             if exchange is not None else
+                             "by NCCL after the GEMM (NCCL_ALGO/NCCL_PROTO pinned)")}[mode],
             "rank_extents": extents,
             "l2": ("inputs larger than L2 per step (A+B+C = %.0f MB > 126 MB), steps back to "
                    "back" % (ws_bytes / 2**20)) if not small else
@@ -527,25 +763,19 @@ def main() -> int:
                    "operands and output (%.0f MB >= 2 x L2), so every step reads its inputs "
                    "from HBM; steps back to back" % (ws_bytes / 2**20, n_rot,
                                                       n_rot * ws_bytes / 2**20)),
+            "operand_generation_s": round(t_gen, 2),
         },
-        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s",
-                "h2d_bytes_per_step": int((info["left"] + info["right"]) * 8),
-                "d2h_bytes_per_step": int(info["output"] * 8 // (world if collective else 1)),
-                "steps": n_e2e, "rounds_ms_per_step": [round(r, 4) for r in rounds],
-                "api": ("tcf_run_streamed_async: H2D / DMMA / D2H overlapped over %d slabs, "
-                        "successive steps pipelined, tcf_sync at the end (include/tcf.h)"
-                        % slabs_used) if collective is None else
-                       ("tcf_upload + tcf_run_scattered into the peer window + tcb_peer_reduce"
-                        " + D2H of the rank's block" if exchange is not None else
-                        "tcf_upload + tcf_run + tcb_reduce_scatter (NCCL) + D2H of the rank's "
-                        "block")},
+        "parity": parity,
+        "parity_ok": bool(parity["ranks_ok"]),
+        "e2e": e2e,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 3),
                      "peak": round(peak.value, 3), "unit": "TFLOP/s",
                      "frac": round(achieved / peak.value, 4), "traffic": None,
                      "kernel": "dgemm_dmma_kernel" if gemm_info.path in (0, 1) else "gemv",
                      "kernel_ms": round(kern_ms, 6),
                      "peak_source": "tcb_fp64_peak: DMMA m8n8k4 register-resident microbenchmark "
-                                    "run live on this GPU (MEASURED_PEAKS.json has no fp64 entry)",
+                                    "run live on this GPU (MEASURED_PEAKS.json has no fp64 "
+                                    "entry) — of builder-measured",
                      "algorithmic_flops_per_launch": flops},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -555,21 +785,20 @@ def main() -> int:
         line["roofline"]["peak_nominal"] = round(
             148 * 128 * float(clk["sm_max_mhz"]) * 1e6 / 1e12, 3)
     prof = ROOT / "profiles" / f"ncu_{cfg}_summary.json"
-    if prof.exists():
+    if prof.exists() and world == 1:
         try:
             line["roofline"]["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        workers = os.cpu_count() or 1
-        secs, kind, cores = cpu_reference(expr, extents, reps=3, workers=workers)
-        if secs:
-            line["cpu_baseline"] = {"value": round(flops / secs / 1e9, 3), "unit": "GFLOP/s",
-                                    "cores": cores, "kind": kind,
-                                    "sample": f"full {cfg} contraction, median of 3 after 1 "
-                                              f"warm-up, tc::execute workers={cores}"}
+        cb = cpu_baseline(cfg)
+        if cb:
+            line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if exchange is not None:
+        barrier()
+        exchange.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0

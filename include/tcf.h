@@ -54,6 +54,13 @@ int tcf_lower(const char* expr, int positional, const char* extents, char* buf, 
 /* Fill `out` with Tensor::seeded_random's stream (src/tensor.cpp:54-62). */
 int tcf_seeded(int64_t n, uint64_t seed, double* out);
 
+/* The block of Tensor::seeded_random's stream (extents ext[0..rank), first
+ * mode fastest) where mode `mode` lies in [lo, hi), dense in the same mode
+ * order: a rank's slab of a seeded operand without materialising the whole
+ * tensor (the stream is still drawn up to the block's end). */
+int tcf_seeded_block(uint64_t seed, int rank, const int64_t* ext, int mode, int64_t lo,
+                     int64_t hi, double* out);
+
 /* Prepared contraction bound to device buffers (tc::PreparedContraction). */
 int tcf_prepare(const char* expr, int positional, const char* extents, int device,
                 void** handle, char* err, int64_t errcap);

@@ -158,6 +158,17 @@ def seeded(n: int, seed: int) -> np.ndarray:
     return out
 
 
+def seeded_block(extents, seed: int, mode: int, lo: int, hi: int) -> np.ndarray:
+    """Slab [lo, hi) along `mode` of Tensor::seeded_random(extents, seed), in
+    storage order (column-major, first mode fastest)."""
+    n = int(np.prod(extents)) // int(extents[mode]) * (hi - lo)
+    out = np.empty(n)
+    arr = (C.c_int64 * len(extents))(*[int(e) for e in extents])
+    rc = native.front().tcf_seeded_block(seed, len(extents), arr, mode, lo, hi, out.ctypes.data)
+    _err(rc, None)
+    return out
+
+
 class Prepared:
     """tc::PreparedContraction: lowered once, device buffers bound."""
 

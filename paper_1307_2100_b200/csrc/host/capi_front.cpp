@@ -228,6 +228,31 @@ int tcf_seeded(int64_t n, uint64_t seed, double* out) {
   return 0;
 }
 
+int tcf_seeded_block(uint64_t seed, int rank, const int64_t* ext, int mode, int64_t lo,
+                     int64_t hi, double* out) {
+  if (rank < 1 || mode < 0 || mode >= rank || !ext || !out) {
+    g_err = "tcf_seeded_block: bad arguments";
+    return 1;
+  }
+  int64_t below = 1, outer = 1;
+  for (int m = 0; m < mode; ++m) below *= ext[m];
+  for (int m = mode + 1; m < rank; ++m) outer *= ext[m];
+  const int64_t e = ext[mode];
+  if (lo < 0 || hi > e || lo >= hi) {
+    g_err = "tcf_seeded_block: empty or out-of-range block";
+    return 1;
+  }
+  std::mt19937_64 gen(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);  // one draw per value
+  double* o = out;
+  for (int64_t q = 0; q < outer; ++q) {
+    gen.discard(static_cast<unsigned long long>(below * lo));
+    for (int64_t i = 0; i < below * (hi - lo); ++i) *o++ = u(gen);
+    if (q + 1 < outer) gen.discard(static_cast<unsigned long long>(below * (e - hi)));
+  }
+  return 0;
+}
+
 int tcf_prepare(const char* expr, int positional, const char* extents, int device, void** handle,
                 char* err, int64_t errcap) {
   try {

@@ -116,6 +116,7 @@ TCF_API = {
                                P_f64, cp, i64]),
     "tcf_lower": (i32, [cp, i32, cp, cp, i64]),
     "tcf_seeded": (i32, [i64, C.c_uint64, vp]),
+    "tcf_seeded_block": (i32, [C.c_uint64, i32, P_i64, i32, i64, i64, vp]),
     "tcf_prepare": (i32, [cp, i32, cp, i32, C.POINTER(vp), cp, i64]),
     "tcf_upload": (i32, [vp, vp, vp]),
     "tcf_run": (i32, [vp]),
