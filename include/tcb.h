@@ -38,6 +38,8 @@ typedef enum tcb_status {
 int tcb_init(int device);
 int tcb_finalize(void);
 int tcb_device_count(int* count);
+/* The device the calling thread's tcb_* calls use (-1 before tcb_init). */
+int tcb_current_device(int* device);
 const char* tcb_last_error(void);
 /* Run subsequent work of this thread on a caller-owned cudaStream_t (passed as
  * void*); NULL restores the context's own stream. */

@@ -12,13 +12,27 @@
 
 namespace tcb {
 
+namespace {
+struct ThreadCtx {
+  int device = -1;  // bound by tcb_init (or lazily to 0)
+  ThreadState per[kMaxDevices];
+  std::string err;
+};
+ThreadCtx& ctx() {
+  static thread_local ThreadCtx c;
+  return c;
+}
+}  // namespace
+
 ThreadState& state() {
-  static thread_local ThreadState st;
-  return st;
+  ThreadCtx& c = ctx();
+  return c.per[c.device < 0 ? 0 : c.device];
 }
 
+std::string& thread_error() { return ctx().err; }
+
 int set_error(int code, const std::string& msg) {
-  state().err = msg;
+  ctx().err = msg;
   return code;
 }
 
@@ -39,9 +53,9 @@ int num_sms() {
 }
 
 int ensure_init() {
-  ThreadState& st = state();
-  if (st.device >= 0) {
-    TCB_CUDA(cudaSetDevice(st.device));
+  const int dev = ctx().device;
+  if (dev >= 0) {
+    TCB_CUDA(cudaSetDevice(dev));
     return TCB_OK;
   }
   return tcb_init(0);
@@ -60,26 +74,20 @@ using namespace tcb;
 extern "C" {
 
 int tcb_init(int device) {
-  ThreadState& st = state();
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
   if (n == 0) return set_error(TCB_ECUDA, "no CUDA device visible");
   if (device < 0 || device >= n) return set_error(TCB_EINVAL, "tcb_init: device out of range");
+  if (device >= kMaxDevices) return set_error(TCB_EUNSUPPORTED, "tcb_init: device index above 15");
   TCB_CUDA(cudaSetDevice(device));
-  if (st.device != device) {
-    if (st.own_stream) cudaStreamDestroy(st.own_stream);
-    if (st.ev0) cudaEventDestroy(st.ev0);
-    if (st.ev1) cudaEventDestroy(st.ev1);
-    st.own_stream = nullptr;
-    st.ev0 = st.ev1 = nullptr;
-    st.ws = nullptr;
-    st.ws_bytes = 0;
-    st.counters = nullptr;
-    st.counters_n = 0;
+  ctx().device = device;
+  ThreadState& st = state();
+  if (!st.own_stream) {  // first use of this device by this thread
     TCB_CUDA(cudaStreamCreateWithFlags(&st.own_stream, cudaStreamNonBlocking));
     TCB_CUDA(cudaEventCreate(&st.ev0));
     TCB_CUDA(cudaEventCreate(&st.ev1));
+    TCB_CUDA(cudaEventCreateWithFlags(&st.order, cudaEventDisableTiming));
     st.stream = st.own_stream;
     st.device = device;
   }
@@ -111,20 +119,26 @@ static cudaMemPool_t device_pool() {
 }
 
 int tcb_finalize(void) {
-  ThreadState& st = state();
-  if (st.device < 0) return TCB_OK;
-  cudaSetDevice(st.device);
-  if (st.stream) cudaStreamSynchronize(st.stream);
-  if (cudaMemPool_t pool = device_pool()) {  // hand cached blocks back to the driver
-    cudaDeviceSynchronize();
-    cudaMemPoolTrimTo(pool, 0);
+  // releases the calling thread's state on every device it used
+  ThreadCtx& c = ctx();
+  for (int d = 0; d < kMaxDevices; ++d) {
+    ThreadState& st = c.per[d];
+    if (st.device < 0) continue;
+    cudaSetDevice(d);
+    if (st.stream) cudaStreamSynchronize(st.stream);
+    if (cudaMemPool_t pool = device_pool()) {  // hand cached blocks back to the driver
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    if (st.ws) cudaFree(st.ws);
+    if (st.counters) cudaFree(st.counters);
+    if (st.own_stream) cudaStreamDestroy(st.own_stream);
+    if (st.ev0) cudaEventDestroy(st.ev0);
+    if (st.ev1) cudaEventDestroy(st.ev1);
+    if (st.order) cudaEventDestroy(st.order);
+    st = ThreadState{};
   }
-  if (st.ws) cudaFree(st.ws);
-  if (st.counters) cudaFree(st.counters);
-  if (st.own_stream) cudaStreamDestroy(st.own_stream);
-  if (st.ev0) cudaEventDestroy(st.ev0);
-  if (st.ev1) cudaEventDestroy(st.ev1);
-  st = ThreadState{};
+  c.device = -1;
   return TCB_OK;
 }
 
@@ -139,12 +153,26 @@ int tcb_device_count(int* count) {
   return TCB_OK;
 }
 
-const char* tcb_last_error(void) { return state().err.c_str(); }
+int tcb_current_device(int* device) {
+  if (!device) return set_error(TCB_EINVAL, "tcb_current_device: null pointer");
+  *device = ctx().device;
+  return TCB_OK;
+}
+
+const char* tcb_last_error(void) { return ctx().err.c_str(); }
 
 int tcb_set_stream(void* stream) {
   TCB_TRY_INIT();
   ThreadState& st = state();
-  st.stream = stream ? static_cast<cudaStream_t>(stream) : st.own_stream;
+  cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : st.own_stream;
+  if (next != st.stream) {
+    // The thread's stream-K workspace and tile counters assume stream order:
+    // work enqueued from now on waits for what this thread left on the
+    // previous stream, so two stream-K GEMMs of one thread never overlap.
+    TCB_CUDA(cudaEventRecord(st.order, st.stream));
+    TCB_CUDA(cudaStreamWaitEvent(next, st.order, 0));
+  }
+  st.stream = next;
   st.pdl_ok = false;
   return TCB_OK;
 }

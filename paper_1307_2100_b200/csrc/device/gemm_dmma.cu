@@ -1522,9 +1522,10 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
 
   const int grid = streamk ? G : static_cast<int>(std::min<int64_t>(tiles, sms));
-  // Programmatic dependent launch when the previous operation on our own
-  // stream was a GEMM whose output does not overlap this one's operands
-  // (read before griddepcontrol.wait). TCB_NO_PDL=1 disables it.
+  // Programmatic dependent launch when the operations on our own stream since
+  // the last serialized launch are all GEMMs and none of their outputs
+  // overlaps this one's operands (read before griddepcontrol.wait).
+  // TCB_NO_PDL=1 disables it.
   static const bool no_pdl = getenv("TCB_NO_PDL") != nullptr;
   const auto [alo, ahi] = operand_range(d, A, true);
   const auto [blo, bhi] = operand_range(d, B, false);
@@ -1560,10 +1561,12 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
   ++st.launches;
   {
+    // outputs of the PDL chain: a fully serialized launch starts a new chain
+    // (everything before it has completed); a PDL launch extends it
     const auto [clo, chi] = output_range(d, C);
+    st.pdl_lo = pdl ? std::min(st.pdl_lo, clo) : clo;
+    st.pdl_hi = pdl ? std::max(st.pdl_hi, chi) : chi;
     st.pdl_ok = true;
-    st.pdl_lo = clo;
-    st.pdl_hi = chi;
   }
   if (trace) {
     note_stream_op();

@@ -11,8 +11,10 @@
 
 namespace tcb {
 
-// Per host-thread state: the device this thread drives, its stream, a grow-only
-// workspace (split-K partials + per-tile counters) and the last error text.
+// Per (host thread, device) state: the device's stream for this thread, a
+// grow-only workspace (split-K partials + per-tile counters), PDL bookkeeping.
+// A thread that alternates between devices (tcb_init(d) before each call)
+// keeps one of these per device, so nothing is dropped or leaked on a switch.
 struct ThreadState {
   int device = -1;
   cudaStream_t own_stream = nullptr;
@@ -25,20 +27,24 @@ struct ThreadState {
   int last_splits = 0;             // (G, tiles, kblocks) of the last stream-K launch
   int64_t last_tiles = 0;
   int64_t last_kblocks = 0;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // tcb_timer_start / tcb_timer_stop
+  cudaEvent_t order = nullptr;                // tcb_set_stream's hand-over
   int64_t launches = 0;
-  // Programmatic dependent launch: true while the last operation enqueued on
-  // the thread's own stream was a DMMA GEMM writing [pdl_lo, pdl_hi); the next
-  // GEMM may then start its prologue and main loop before that one finishes
-  // (it waits for it before any global write). Every other stream operation
-  // clears it.
+  // Programmatic dependent launch: true while the operations enqueued on the
+  // thread's own stream since the last fully serialized launch are all DMMA
+  // GEMMs (a PDL chain). [pdl_lo, pdl_hi) covers the union of their outputs:
+  // a GEMM launched with PDL may issue its operand loads while ANY earlier
+  // GEMM of the chain still runs (each one lets its dependent start once its
+  // own CTAs are resident), so its operands must avoid every output of the
+  // chain, not just the last one. Every other stream operation clears it.
   bool pdl_ok = false;
   uintptr_t pdl_lo = 0, pdl_hi = 0;
   tcb_gemm_info last_info{};
-  std::string err;
 };
 
-ThreadState& state();
+constexpr int kMaxDevices = 16;
+ThreadState& state();            // the calling thread's state for its current device
+std::string& thread_error();     // the calling thread's last error text
 int set_error(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int ensure_init();  // lazily binds device 0 when tcb_init was not called

@@ -104,7 +104,7 @@ constexpr std::int64_t kChunk = 16LL << 20;
 constexpr int kBuffers = 3;
 constexpr std::int64_t kDirect = 4LL << 20;  // below this the driver's copy is fine
 
-// Bounce buffers and their "free again" events, one set per host thread.
+// Bounce buffers and their "free again" events.
 struct Bounce {
   void* buf[kBuffers] = {};
   void* ev[kBuffers] = {};
@@ -126,10 +126,15 @@ CopyPool& pool() {
   static CopyPool p;
   return p;
 }
+// one set per (thread, device): the events belong to the device they were
+// created on, and a thread may alternate between devices
 Bounce& bounce() {
-  thread_local Bounce b;
-  b.ensure();
-  return b;
+  thread_local Bounce b[16];
+  int dev = 0;
+  tcb_current_device(&dev);
+  Bounce& mine = b[dev < 0 ? 0 : dev & 15];
+  mine.ensure();
+  return mine;
 }
 
 bool pinned(const void* p) {

@@ -50,6 +50,7 @@ TCB_API = {
     "tcb_init": (i32, [i32]),
     "tcb_finalize": (i32, []),
     "tcb_device_count": (i32, [C.POINTER(C.c_int)]),
+    "tcb_current_device": (i32, [C.POINTER(C.c_int)]),
     "tcb_last_error": (cp, []),
     "tcb_set_stream": (i32, [vp]),
     "tcb_sync": (i32, []),
