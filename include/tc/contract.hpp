@@ -424,11 +424,29 @@ double max_rel_error(const Tensor& a, const Tensor& b);
 /// ||a-b||_F / ||b||_F — the BASELINE parity criterion (not in the reference).
 double rel_frobenius_error(const Tensor& a, const Tensor& b);
 
-/// Thrown by execute_all_slicings when the sweep exceeds its work cap
-/// (the reference declares it in tc/oracle.hpp:11-13).
+/// Thrown by execute_all_slicings and contract_naive when the work exceeds
+/// the cap (the reference declares it in tc/oracle.hpp:11-13; tc/oracle.hpp
+/// here includes this header).
 struct resource_limit_error : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+
+// ------------------------------------------------ oracle API (tc/oracle.hpp)
+// reference: include/tc/oracle.hpp:15-25
+
+struct OracleStats {
+  std::int64_t multiply_adds = 0;
+};
+
+/// Direct nested summation in a fixed lexicographic order: for every output
+/// coordinate (free labels in output order), left*right summed over the full
+/// range of the contracted labels (left-mode order, first fastest), from 0.
+/// Evaluated on the device by tcb_contract_naive with separately rounded
+/// products and sums: bit-identical to the reference's src/oracle.cpp:32-94.
+/// Refuses jobs above the work cap (resource_limit_error). A verification
+/// API (the CLI's --verify in the reference); execute() never uses it.
+Tensor contract_naive(const ValidatedContraction& v, const Tensor& left, const Tensor& right,
+                      std::int64_t work_cap = 1000000000, OracleStats* stats = nullptr);
 
 // ============================================================ device recipe
 // (new; no reference counterpart) — the lowering of a contraction onto the

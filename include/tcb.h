@@ -176,6 +176,17 @@ int tcb_ddot(int64_t k, const double* x, int64_t incx, const double* y, int64_t 
  * in the given dimension order (first fastest). Replaces the executor's
  * per-slice packing copy (materialize, src/executor.cpp:41-59) with one
  * coalesced launch over the whole operand. */
+/* The reference's brute-force oracle (tc::contract_naive, src/oracle.cpp:32-94)
+ * on device buffers: O[free] = sum over the contracted labels (LEFT-mode
+ * order, first fastest) of L*R, free labels in OUTPUT order (first fastest),
+ * products and sums rounded separately (no FMA) — bit-identical to the
+ * reference built with its own flags. Per label: extent and element strides
+ * into L, R, O (0 where the label does not address a tensor). A verification
+ * path behind tc/oracle.hpp; execute() never uses it. */
+int tcb_contract_naive(int nfree, const int64_t* fext, const int64_t* fls, const int64_t* frs,
+                       const int64_t* fos, int ncon, const int64_t* cext, const int64_t* cls,
+                       const int64_t* crs, const double* L, const double* R, double* O);
+
 int tcb_permute(int rank, const int64_t* ext, const int64_t* src_str, const double* src,
                 double* dst);
 

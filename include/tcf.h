@@ -45,6 +45,13 @@ int tcf_execute_host(const char* expr, int positional, const char* extents, cons
                      int kernel, const char* s_left, const char* s_right, int64_t* stats,
                      double* seconds, char* err, int64_t errcap);
 
+/* tc::contract_naive (reference include/tc/oracle.hpp:21-23) on operands
+ * seeded like tcf_execute: the brute-force sum on the device, bit-identical
+ * to the reference's oracle. *macs = multiply-adds; status 3 above work_cap. */
+int tcf_contract_naive(const char* expr, int positional, const char* extents, uint64_t seed,
+                       int64_t work_cap, double* out, int64_t out_cap, int64_t* macs, char* err,
+                       int64_t errcap);
+
 /* The device recipe (lowering) of a contraction, without touching a device:
  * "L1|L2|L3 gemm m=.. n=.. k=.. a(sm,sk) b(sk,sn) batch=[..] permutes=N", or
  * "L4 gemm m=.. n=.. k=.. m[ext:str,..] n[..] k[ext:str_a/str_b,..] ..." for

@@ -112,6 +112,23 @@ def execute_host(expr: str, extents: str, left: np.ndarray, right: np.ndarray,
             "flops": stats[3], "wall_seconds": secs.value}
 
 
+def contract_naive(expr: str, extents: str, seed: int = 1, positional: bool = False,
+                   work_cap: int = 1000000000):
+    """tc::contract_naive (tc/oracle.hpp) on seeded operands, evaluated on the
+    device: (result, multiply-adds). MemoryError above work_cap."""
+    out_l, _, _ = parse_expr(expr)
+    ext = dict(kv.split("=") for kv in extents.split(",") if kv)
+    n = int(np.prod([int(ext[x]) for x in out_l])) if out_l else 1
+    out = np.zeros(n)
+    macs = C.c_int64()
+    err = C.create_string_buffer(4096)
+    rc = native.front().tcf_contract_naive(expr.encode(), int(positional), extents.encode(), seed,
+                                           work_cap, out.ctypes.data, n, C.byref(macs), err,
+                                           len(err))
+    _err(rc, err)
+    return out, macs.value
+
+
 def tensor_text(extents, variance: str, seed: int, name: str = "t") -> str:
     """TENSOR v1 text (tc::write_tensor) of Tensor::seeded_random(extents,
     variance, seed, name)."""

@@ -209,6 +209,25 @@ int tcf_execute_host(const char* expr, int positional, const char* extents, cons
   TCF_GUARD(err, errcap)
 }
 
+int tcf_contract_naive(const char* expr, int positional, const char* extents, uint64_t seed,
+                       int64_t work_cap, double* out, int64_t out_cap, int64_t* macs, char* err,
+                       int64_t errcap) {
+  try {
+    const tc::ContractionSpec spec = tc::parse(expr ? expr : "", positional != 0);
+    const Shapes s = shapes_of(spec, parse_extents(extents));
+    const tc::Tensor left = tc::Tensor::seeded_random(s.le, s.lv, seed, spec.left.name);
+    const tc::Tensor right = tc::Tensor::seeded_random(s.re, s.rv, seed + 1, spec.right.name);
+    const tc::ValidatedContraction v = tc::validate(spec, left, right);
+    tc::OracleStats st;
+    const tc::Tensor res = tc::contract_naive(v, left, right, work_cap, &st);
+    if (res.size() > out_cap) throw std::invalid_argument("output buffer too small");
+    std::memcpy(out, res.data(), static_cast<std::size_t>(res.size()) * 8);
+    if (macs) *macs = st.multiply_adds;
+    return 0;
+  }
+  TCF_GUARD(err, errcap)
+}
+
 int tcf_lower(const char* expr, int positional, const char* extents, char* buf, int64_t cap) {
   try {
     const tc::ContractionSpec spec = tc::parse(expr ? expr : "", positional != 0);

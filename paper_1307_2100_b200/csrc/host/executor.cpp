@@ -1172,6 +1172,44 @@ std::vector<SlicingRun> execute_all_slicings(const ValidatedContraction& v, cons
   return runs;
 }
 
+// tc/oracle.hpp (reference include/tc/oracle.hpp:11-25): the brute-force
+// contraction evaluated by the device kernel tcb_contract_naive, bit-identical
+// to the reference's src/oracle.cpp:32-94 (same order, no FMA).
+Tensor contract_naive(const ValidatedContraction& v, const Tensor& left, const Tensor& right,
+                      std::int64_t work_cap, OracleStats* stats) {
+  std::int64_t work = 1;
+  for (const LabelInfo& l : v.labels) work *= l.extent;
+  if (work > work_cap)
+    throw resource_limit_error("oracle work exceeds cap: " + std::to_string(work) +
+                               " multiply-adds");
+  Tensor out(v.output_extents(), v.output_variance(), v.spec.output.name);
+  std::vector<std::int64_t> fe, fl, fr, fo, ce, cl, cr;
+  for (const auto& ix : v.spec.output.indices) {
+    const LabelInfo& li = v.labels[static_cast<std::size_t>(v.label_index(ix.label))];
+    fe.push_back(li.extent);
+    fl.push_back(li.left_mode >= 0 ? stride_of(left, li.left_mode) : 0);
+    fr.push_back(li.right_mode >= 0 ? stride_of(right, li.right_mode) : 0);
+    fo.push_back(stride_of(out, li.output_mode));
+  }
+  for (int id : v.contracted) {
+    const LabelInfo& li = v.labels[static_cast<std::size_t>(id)];
+    ce.push_back(li.extent);
+    cl.push_back(stride_of(left, li.left_mode));
+    cr.push_back(stride_of(right, li.right_mode));
+  }
+  DevBuf dl(std::max<std::int64_t>(left.size(), 1) * 8), dr(std::max<std::int64_t>(right.size(), 1) * 8),
+      dout(out.size() * 8);
+  check(tcb_h2d(dl.p, left.data(), left.size() * 8), "oracle upload");
+  check(tcb_h2d(dr.p, right.data(), right.size() * 8), "oracle upload");
+  check(tcb_contract_naive(static_cast<int>(fe.size()), fe.data(), fl.data(), fr.data(),
+                           fo.data(), static_cast<int>(ce.size()), ce.data(), cl.data(),
+                           cr.data(), dl.d(), dr.d(), dout.d()),
+        "contract_naive");
+  check(tcb_d2h(out.data(), dout.p, out.size() * 8), "oracle download");
+  if (stats) stats->multiply_adds = work;
+  return out;
+}
+
 std::uint64_t tensor_hash(const Tensor& t) {
   // FNV-1a over the little-endian bytes of each element (src/executor.cpp:371-383)
   std::uint64_t h = 0xcbf29ce484222325ull;

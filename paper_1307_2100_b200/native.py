@@ -86,6 +86,8 @@ TCB_API = {
     "tcb_dger": (i32, [i64, i64, f64, vp, i64, vp, i64, vp, i64]),
     "tcb_ddot": (i32, [i64, vp, i64, vp, i64, P_f64]),
     "tcb_permute": (i32, [i32, P_i64, P_i64, vp, vp]),
+    "tcb_contract_naive": (i32, [i32, P_i64, P_i64, P_i64, P_i64, i32, P_i64, P_i64, P_i64, vp,
+                                 vp, vp]),
     "tcb_comm_version": (i32, [C.POINTER(C.c_int)]),
     "tcb_comm_unique_id": (i32, [vp]),
     "tcb_comm_init": (i32, [i32, i32, vp, C.POINTER(vp)]),
@@ -115,6 +117,7 @@ TCF_API = {
                           P_f64, cp, i64]),
     "tcf_execute_host": (i32, [cp, i32, cp, vp, vp, vp, i64, i32, i32, i32, cp, cp, P_i64,
                                P_f64, cp, i64]),
+    "tcf_contract_naive": (i32, [cp, i32, cp, C.c_uint64, i64, vp, i64, P_i64, cp, i64]),
     "tcf_lower": (i32, [cp, i32, cp, cp, i64]),
     "tcf_seeded": (i32, [i64, C.c_uint64, vp]),
     "tcf_seeded_block": (i32, [C.c_uint64, i32, P_i64, i32, i64, i64, vp]),

@@ -1,10 +1,14 @@
 // Executor and backend suites restated from the reference's doctest files
 // (tests/test_executor.cpp, tests/test_kernels.cpp) against the engine's
 // device path: tc::execute with make_backend("b200"). Requires a B200.
+#include <cstring>
 #include <random>
 
 #include "harness.hpp"
 #include "helpers.hpp"
+#include "tc/executor.hpp"
+#include "tc/kernels.hpp"
+#include "tc/oracle.hpp"
 
 using namespace tc;
 using tst::bind_expr;
@@ -135,6 +139,17 @@ TEST_CASE("device faults surface with the contraction attached") {  // :240-291
     CHECK(what.find("synthetic device fault") != std::string::npos);
     CHECK(what.find("R[+a,-e]") != std::string::npos);
   }
+}
+
+TEST_CASE("tc/oracle.hpp: contract_naive equals the direct sum, refuses above its cap") {
+  const auto b = bind_expr("R[+a,+b,+c,+d] = X[+i,+a,+j,+b] * Y[-j,+c,-i,+d]",
+                           {{"a", 2}, {"b", 3}, {"c", 2}, {"d", 3}, {"i", 2}, {"j", 3}});
+  OracleStats st;
+  const Tensor got = contract_naive(b.v, b.left, b.right, 1000000000, &st);
+  const Tensor want = naive(b.v, b.left, b.right);
+  CHECK(std::memcmp(got.data(), want.data(), static_cast<std::size_t>(got.size()) * 8) == 0);
+  CHECK(st.multiply_adds == 2 * 3 * 2 * 3 * 2 * 3);
+  CHECK_THROWS_AS(contract_naive(b.v, b.left, b.right, 10), resource_limit_error);
 }
 
 TEST_CASE("backend gemm/gemv/ger/dot known answers on host pointers") {  // test_kernels.cpp
