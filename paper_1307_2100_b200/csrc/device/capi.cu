@@ -132,6 +132,7 @@ int tcb_finalize(void) {
     }
     if (st.ws) cudaFree(st.ws);
     if (st.counters) cudaFree(st.counters);
+    if (st.pace) cudaFree(st.pace);
     if (st.own_stream) cudaStreamDestroy(st.own_stream);
     if (st.ev0) cudaEventDestroy(st.ev0);
     if (st.ev1) cudaEventDestroy(st.ev1);

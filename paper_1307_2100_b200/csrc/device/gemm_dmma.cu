@@ -128,6 +128,26 @@ struct Params {
   // coordinate program pc (sources: 0 m origin, 1 n origin, 2 batch)
   int c_tma;
   MapProg pc;
+  // tile raster: groups of `raster_g` m-tiles per n sweep (raster_n = 0), or
+  // of raster_g n-tiles per m sweep (raster_n = 1, keeps that set of B panels
+  // resident in L2 while A streams)
+  int raster_g, raster_n;
+  // k-pacing (long-k launches): the producers of all CTAs announce every
+  // 2^pace_shift issued k-blocks on one global counter and do not start
+  // epoch e before every CTA has announced epoch e - pace_slack, so the CTAs
+  // that share an operand panel stay within a few epochs of each other and
+  // its k-slices are fetched from DRAM once, then hit in L2. The counter is
+  // monotonic across launches: this launch's announcements start at
+  // pace_base and total pace_total per CTA. A performance hint only: a wait
+  // gives up after a timeout, so it never blocks progress.
+  unsigned long long* pace;
+  unsigned long long pace_base;
+  int pace_shift, pace_slack, pace_grid;
+  unsigned pace_total;
+  // whole tiles of odd waves issue their k-blocks in descending order: the
+  // k-slices a wave used last are the next wave's first, still in L2 (the
+  // consumers are order-agnostic; the tile's sum order is fixed per tile)
+  int kflip;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -257,14 +277,20 @@ __device__ __forceinline__ Unit decode_unit(const Params& p, int64_t tile) {
   const unsigned per_batch = static_cast<unsigned>(p.tiles_m) * static_cast<unsigned>(p.tiles_n);
   r.batch = t / per_batch;
   const unsigned tt = t - r.batch * per_batch;
-  // grouped raster: 8 m-tiles share each n-tile sweep (L2 reuse of B)
-  const unsigned group_span = 8u * static_cast<unsigned>(p.tiles_n);
+  // grouped raster: raster_g m-tiles share each n-tile sweep (L2 reuse of B
+  // panels across the group), or with raster_n raster_g n-tiles share each
+  // m-tile sweep (a resident set of B panels while A streams through)
+  const int G = p.raster_g;
+  const int lead = p.raster_n ? p.tiles_n : p.tiles_m;
+  const unsigned cross = static_cast<unsigned>(p.raster_n ? p.tiles_m : p.tiles_n);
+  const unsigned group_span = static_cast<unsigned>(G) * cross;
   const unsigned g = tt / group_span;
-  const int first_m = static_cast<int>(g * 8u);
-  const unsigned gsize = static_cast<unsigned>(min(8, p.tiles_m - first_m));
+  const int first = static_cast<int>(g * static_cast<unsigned>(G));
+  const unsigned gsize = static_cast<unsigned>(min(G, lead - first));
   const unsigned w = tt - g * group_span;
-  r.tm = first_m + static_cast<int>(w % gsize);
-  r.tn = static_cast<int>(w / gsize);
+  const int a = first + static_cast<int>(w % gsize), b = static_cast<int>(w / gsize);
+  r.tm = p.raster_n ? b : a;
+  r.tn = p.raster_n ? a : b;
   return r;
 }
 
@@ -366,6 +392,33 @@ __device__ __forceinline__ int sk_owner(const Params& p, int pos) {
   return lo;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// k-pacing (see Params): announce that epoch e - 1 is issued, then wait (at
+// most ~40 us; after a timeout the CTA stops waiting for the rest of the
+// launch) until every CTA has announced epoch e - pace_slack.
+__device__ __forceinline__ void pace_epoch(const Params& p, uint32_t e, bool& wait_ok) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(p.pace) : "memory");
+  if (!wait_ok || e < static_cast<uint32_t>(p.pace_slack)) return;
+  const unsigned long long target =
+      p.pace_base + static_cast<unsigned long long>(e - p.pace_slack + 1) * p.pace_grid;
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.pace) : "memory");
+  if (v >= target) return;
+  const unsigned long long t0 = global_ns();
+  do {
+    __nanosleep(128);
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.pace) : "memory");
+    if (global_ns() - t0 > 40000) {
+      wait_ok = false;
+      return;
+    }
+  } while (v < target);
+}
+
 // Producer-side iterator over this CTA's (segment, k-block) sequence. All
 // per-segment address math happens once per segment here, in the producer
 // warpgroup, never on the consumer warps.
@@ -376,6 +429,7 @@ struct LoadIter {
   int m0, n0;            // tile origin (TMA coordinates are int32)
   int64_t oa, ob;        // batch offsets (cp.async path)
   int ca[5], cb[5];      // TMA: outer + batch coordinates of the segment's tile
+  int mirror;            // >= 0: k-blocks issued as mirror - kb (descending)
   bool valid;
 
   template <bool USE_TMA>
@@ -388,6 +442,10 @@ struct LoadIter {
     int64_t tile;
     valid = it.next(p, tile, kb, kb1);
     if (!valid) return;
+    mirror = (p.kflip && kb == 0 && kb1 == p.kblocks &&
+              ((static_cast<unsigned>(tile) / gridDim.x) & 1u))
+                 ? kb1 - 1
+                 : -1;
     const Unit un = decode_unit(p, tile);
     m0 = un.tm * BM;
     n0 = un.tn * BN;
@@ -422,7 +480,7 @@ template <bool A_KMAJOR, bool B_KMAJOR, bool USE_TMA, typename Iter>
 __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& tmA,
                                             const CUtensorMap& tmB, const Iter& li,
                                             uint32_t sA, uint32_t full, int ptid) {
-  const int k0 = li.kb * BK;
+  const int k0 = (li.mirror >= 0 ? li.mirror - li.kb : li.kb) * BK;
   const uint32_t sB = sA + STAGE_A;
   if (USE_TMA) {
     mbar_expect_tx(full, STAGE_BYTES);
@@ -647,8 +705,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     LoadIter<SPLITK> li;
     li.template start<USE_TMA>(p);
     uint32_t g = 0;
+    const bool pacing = USE_TMA && p.pace != nullptr;
+    const uint32_t pace_mask = (1u << p.pace_shift) - 1u;
+    bool pace_wait = true;
+    uint32_t announced = 0;
 #pragma unroll 1
     while (li.valid) {
+      if (pacing && g != 0 && (g & pace_mask) == 0) {
+        pace_epoch(p, g >> p.pace_shift, pace_wait);
+        ++announced;
+      }
       const uint32_t s = g % NST;
       mbar_wait(empty0 + 8 * s, ((g / NST) & 1) ^ 1);
       if (USE_TMA && (p.diag & 8) && g >= static_cast<uint32_t>(NST))
@@ -659,6 +725,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       ++g;
       li.template advance<USE_TMA>(p);
     }
+    if (pacing && p.pace_total > announced)  // the epochs this CTA never runs
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p.pace),
+                   "l"(static_cast<unsigned long long>(p.pace_total - announced))
+                   : "memory");
     if (!USE_TMA) asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
@@ -1361,6 +1431,29 @@ int check_gemm_groups(const tcb_gemm_desc& d) {
   return TCB_OK;
 }
 
+// The thread's k-pacing counter, zeroed (stream-ordered) when first used or
+// after a failed launch left its base unknown.
+bool make_pace_ready(ThreadState& st) {
+  if (!st.pace) {
+    if (cudaMalloc(&st.pace, sizeof(unsigned long long)) != cudaSuccess) {
+      cudaGetLastError();
+      st.pace = nullptr;
+      return false;
+    }
+    st.pace_reset = true;
+  }
+  if (st.pace_reset) {
+    note_stream_op();
+    if (cudaMemsetAsync(st.pace, 0, sizeof(unsigned long long), st.stream) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    st.pace_base = 0;
+    st.pace_reset = false;
+  }
+  return true;
+}
+
 int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C) {
   ThreadState& st = state();
   Params p{};
@@ -1422,8 +1515,13 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       if (G <= tiles) G = 1;
     } else if (sms <= SK_MAX) {
       const int64_t waves = tiles / sms, rem = tiles % sms;
-      // TCB_SK_WASTE: idle-fraction threshold of the hybrid (diagnostics; default 0.05)
-      static const double waste = getenv("TCB_SK_WASTE") ? atof(getenv("TCB_SK_WASTE")) : 0.05;
+      // TCB_SK_WASTE: idle-fraction threshold of the hybrid (diagnostics). The
+      // hybrid's data-parallel phase stores C without the staged epilogue,
+      // which costs short-k tiles a few per cent (cfg2 12 %, cfg3 2 %): 5 %
+      // by default, 0.4 % for tiles of >= 2048 k-blocks, whose epilogue is
+      // negligible (cfg5: 4096 tiles = 27.7 waves, 1.2 % idle in the last one)
+      static const double waste_env = getenv("TCB_SK_WASTE") ? atof(getenv("TCB_SK_WASTE")) : -1;
+      const double waste = waste_env >= 0 ? waste_env : (kblocks >= 2048 ? 0.004 : 0.05);
       if (rem != 0 &&
           static_cast<double>(waves + 1) * sms > (1.0 + waste) * static_cast<double>(tiles) &&
           std::min<int64_t>(sms, rem * kblocks / 4) > rem) {
@@ -1522,6 +1620,77 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
 
   const int grid = streamk ? G : static_cast<int>(std::min<int64_t>(tiles, sms));
+
+  // Tile raster. Default: groups of 8 m-tiles per n sweep. When the operands
+  // exceed L2 but one side's panels (BM or BN rows x K) fit a 64 MB budget in
+  // groups of >= 4, group along the side with fewer tiles and keep that group
+  // of panels resident while the other operand streams through (cfg4: groups
+  // of 16 of B's 32 panels of 4 MB; A's 512 panels are read twice instead of
+  // B being re-read for every group of 8 A panels). TCB_RASTER=m<g>|n<g>
+  // overrides (diagnostics).
+  p.raster_g = 8;
+  p.raster_n = 0;
+  {
+    const int64_t a_panel = static_cast<int64_t>(BM) * d.k * 8;
+    const int64_t b_panel = static_cast<int64_t>(BN) * d.k * 8;
+    const int64_t budget = 64LL << 20;
+    if ((d.m + d.n) * d.k * 8 > (126LL << 20) && a_panel > budget / 4 &&
+        b_panel > budget / 4) {
+      // no panel group fits: k-pacing keeps each wave's panels in L2 one
+      // k-window at a time, so a wave reads (its m-tiles + its n-tiles)
+      // panels; about square waves (12 x 12.3 of 148) minimise that
+      p.raster_g = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.tiles_m, 12)));
+    } else if ((d.m + d.n) * d.k * 8 > (126LL << 20)) {
+      if (p.tiles_m >= p.tiles_n) {
+        const int64_t gn = std::min<int64_t>(p.tiles_n, budget / std::max<int64_t>(1, b_panel));
+        if (gn >= 4 && gn < p.tiles_m) {
+          p.raster_n = 1;
+          p.raster_g = static_cast<int>(gn);
+        }
+      } else {
+        const int64_t gm = std::min<int64_t>(p.tiles_m, budget / std::max<int64_t>(1, a_panel));
+        if (gm >= 8) p.raster_g = static_cast<int>(gm);
+      }
+    }
+    static const char* rs = getenv("TCB_RASTER");
+    if (rs && (rs[0] == 'm' || rs[0] == 'n') && atoi(rs + 1) > 0) {
+      p.raster_n = rs[0] == 'n';
+      p.raster_g = atoi(rs + 1);
+    }
+  }
+
+  // k-pacing (see Params) for long-k launches through TMA: every CTA issues
+  // at least 8 epochs of 32 k-blocks and tiles have >= 128 k-blocks.
+  // TCB_NO_PACE=1 disables it (diagnostics).
+  p.pace = nullptr;
+  p.kflip = 0;
+  {
+    static const bool no_pace = getenv("TCB_NO_PACE") != nullptr;
+    int64_t maxkb = 0;  // most k-blocks any CTA issues
+    if (streamk) {
+      for (int c = 0; c < G; ++c) {
+        const int64_t dpt = c < dp ? (dp - 1 - c) / G + 1 : 0;
+        maxkb = std::max<int64_t>(maxkb, dpt * kblocks + p.sk_start[c + 1] - p.sk_start[c]);
+      }
+    } else {
+      maxkb = (tiles + grid - 1) / grid * kblocks;
+    }
+    // TCB_PACE=<shift>,<slack> (diagnostics): epoch 2^shift k-blocks, slack in epochs
+    static const char* pe = getenv("TCB_PACE");
+    static const int kShift = pe ? std::max(1, atoi(pe)) : 4;
+    static const int kSlack = (pe && strchr(pe, ',')) ? std::max(1, atoi(strchr(pe, ',') + 1)) : 2;
+    if (!no_pace && tma && kblocks >= 128 && maxkb >= (8LL << kShift) &&
+        make_pace_ready(st)) {
+      static const bool no_flip = getenv("TCB_NO_KFLIP") != nullptr;
+      p.kflip = no_flip ? 0 : 1;
+      p.pace = st.pace;
+      p.pace_base = st.pace_base;
+      p.pace_shift = kShift;
+      p.pace_slack = kSlack;
+      p.pace_grid = grid;
+      p.pace_total = static_cast<unsigned>((maxkb + (1 << kShift) - 1) >> kShift);
+    }
+  }
   // Programmatic dependent launch when the operations on our own stream since
   // the last serialized launch are all GEMMs and none of their outputs
   // overlaps this one's operands (read before griddepcontrol.wait).
@@ -1557,9 +1726,11 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   }
   if (e != cudaSuccess) {
     st.last_splits = 0;
+    if (p.pace) st.pace_reset = true;
     return cuda_fail(e, "dgemm_dmma launch");
   }
   ++st.launches;
+  if (p.pace) st.pace_base += static_cast<unsigned long long>(p.pace_total) * grid;
   {
     // outputs of the PDL chain: a fully serialized launch starts a new chain
     // (everything before it has completed); a PDL launch extends it

@@ -27,6 +27,9 @@ struct ThreadState {
   int last_splits = 0;             // (G, tiles, kblocks) of the last stream-K launch
   int64_t last_tiles = 0;
   int64_t last_kblocks = 0;
+  unsigned long long* pace = nullptr;  // k-pacing counter (monotonic across launches)
+  unsigned long long pace_base = 0;    // its value once every earlier launch has finished
+  bool pace_reset = true;              // re-zero before the next paced launch
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // tcb_timer_start / tcb_timer_stop
   cudaEvent_t order = nullptr;                // tcb_set_stream's hand-over
   int64_t launches = 0;
