@@ -1519,7 +1519,9 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       // hybrid's data-parallel phase stores C without the staged epilogue,
       // which costs short-k tiles a few per cent (cfg2 12 %, cfg3 2 %): 5 %
       // by default, 0.4 % for tiles of >= 2048 k-blocks, whose epilogue is
-      // negligible (cfg5: 4096 tiles = 27.7 waves, 1.2 % idle in the last one)
+      // negligible (cfg5: 4096 tiles = 27.7 waves, 1.2 % idle in the last one:
+      // 987.9 -> 973.6 ms). Measured against it: the 256-k-block beta = 1 slab
+      // GEMMs of cfg5's streamed host path lose 2 % with the hybrid.
       static const double waste_env = getenv("TCB_SK_WASTE") ? atof(getenv("TCB_SK_WASTE")) : -1;
       const double waste = waste_env >= 0 ? waste_env : (kblocks >= 2048 ? 0.004 : 0.05);
       if (rem != 0 &&

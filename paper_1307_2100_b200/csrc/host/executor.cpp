@@ -944,7 +944,8 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
                                         int slabs, int label, bool wait) {
   const LabelInfo& kl = v_.labels[static_cast<std::size_t>(label)];
   const std::int64_t E = kl.extent;
-  if (slabs <= 0)  // ~4 MB of operand data per slab, 2..64 slabs
+  const bool auto_slabs = slabs <= 0;
+  if (auto_slabs)  // ~4 MB of operand data per slab, 2..64 slabs
     slabs = static_cast<int>(std::clamp<std::int64_t>((nl_ + nr_) * 8 / (4LL << 20), 2, 64));
   slabs = static_cast<int>(std::min<std::int64_t>(slabs, E));
   int pinned_l = 0, pinned_r = 0, pinned_o = 0;
@@ -973,23 +974,72 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     download(out);
     return 1;
   }
-  std::map<std::int64_t, DeviceRecipe> recipes;  // one per distinct slab extent
+  // Slab extents: a short ramp (1, 2, 4, ... up to the nominal extent) so the
+  // first contraction starts after a small upload instead of a whole nominal
+  // slab's, then nominal slabs (a tail below half the nominal merges into the
+  // slab before it).
+  // An explicit slab count gets equal slabs. Slab offsets stay multiples of 2
+  // when a row is an odd number of doubles (16-byte aligned bases: the tensor
+  // maps of in-place index groups need them).
   std::vector<std::int64_t> sizes;
-  for (int i = 0; i < slabs; ++i) {
-    const std::int64_t e = E / slabs + (i < E % slabs ? 1 : 0);
-    sizes.push_back(e);
-    if (recipes.count(e)) continue;
+  if (!auto_slabs) {
+    for (int i = 0; i < slabs; ++i) sizes.push_back(E / slabs + (i < E % slabs ? 1 : 0));
+  } else {
+    const std::int64_t unit = ((sa | sb) & 1) ? 2 : 1;
+    const std::int64_t nominal = std::max<std::int64_t>(unit, E / slabs / unit * unit);
+    std::int64_t rest = E, ramp = unit;
+    while (rest > 0) {
+      std::int64_t e = std::min({rest, ramp, nominal});
+      if (rest - e > 0 && rest - e < (nominal + 1) / 2) e = rest;
+      sizes.push_back(e);
+      rest -= e;
+      ramp *= 2;
+    }
+    slabs = static_cast<int>(sizes.size());
+  }
+  // The last slab's contraction is split into column blocks of the output's
+  // outermost label, each downloaded as soon as it is final, so the result's
+  // download overlaps the last contractions instead of following them.
+  const auto& outs = v_.spec.output.indices;
+  const int o_label = outs.empty() ? -1 : v_.label_index(outs.back().label);
+  const std::int64_t o_ext = o_label < 0 ? 1 : v_.labels[static_cast<std::size_t>(o_label)].extent;
+  int parts = auto_slabs ? static_cast<int>(std::min<std::int64_t>(8, o_ext)) : 1;
+  std::map<std::pair<std::int64_t, std::int64_t>, DeviceRecipe> recipes;  // (slab, block) extents
+  auto recipe = [&](std::int64_t e, std::int64_t ob) -> const DeviceRecipe* {
+    const auto key = std::make_pair(e, ob);
+    if (auto it = recipes.find(key); it != recipes.end()) return &it->second;
     ValidatedContraction sv = v_;
     sv.labels[static_cast<std::size_t>(label)].extent = e;
+    if (ob > 0) sv.labels[static_cast<std::size_t>(o_label)].extent = ob;
     bool ok = groups_ok_;
     DeviceRecipe r = lower_checked(sv, &ok, &v_);
-    if (!r.permutes.empty()) {  // not expected (the full recipe permutes nothing)
-      upload(left, right);
-      run();
-      download(out);
-      return 1;
-    }
-    recipes.emplace(e, std::move(r));
+    if (!r.permutes.empty()) return nullptr;  // not expected (the full recipe permutes nothing)
+    return &recipes.emplace(key, std::move(r)).first->second;
+  };
+  bool lowered = true;
+  for (std::int64_t e : sizes) lowered = lowered && recipe(e, 0) != nullptr;
+  for (int q = 0; q < parts && parts >= 2; ++q)
+    lowered = lowered && recipe(sizes.back(), o_ext * (q + 1) / parts - o_ext * q / parts);
+  if (!lowered) {
+    upload(left, right);
+    run();
+    download(out);
+    return 1;
+  }
+  // element strides of the output's outermost label in A, B and C
+  std::int64_t o_sa = 0, o_sb = 0, o_sc = 1;
+  if (parts >= 2) {
+    const LabelInfo& li = v_.labels[static_cast<std::size_t>(o_label)];
+    auto stride_in = [&](bool right_side, int mode) {
+      std::int64_t st = 1;
+      for (int m = 0; m < mode; ++m)
+        st *= (right_side ? v_.label_at_right_mode(m) : v_.label_at_left_mode(m)).extent;
+      return st;
+    };
+    if (li.left_mode >= 0) o_sa = stride_in(false, li.left_mode);
+    if (li.right_mode >= 0) o_sb = stride_in(true, li.right_mode);
+    o_sc = no_ / o_ext;
+    if ((o_sa | o_sb | o_sc) & 1) parts = 1;  // block offsets would break 16-byte alignment
   }
   if (!pipes_) pipes_ = std::make_unique<Pipes>();
   Pipes& h = *pipes_;
@@ -1009,15 +1059,34 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     void* ready = h.event();
     check(tcb_event_record(ready, h.up), "event");
     check(tcb_stream_wait_event(compute, ready), "event");
-    tcb_gemm_desc d = desc_of(recipes.at(e));
-    d.beta = s == 0 ? 0.0 : 1.0;
-    check(tcb_gemm(&d, dl_ + e0 * sa, dr_ + e0 * sb, do_), "contraction");
+    const double beta = s == 0 ? 0.0 : 1.0;
+    if (s + 1 < slabs || parts < 2) {
+      tcb_gemm_desc d = desc_of(*recipe(e, 0));
+      d.beta = beta;
+      check(tcb_gemm(&d, dl_ + e0 * sa, dr_ + e0 * sb, do_), "contraction");
+    } else {
+      for (int q = 0; q < parts; ++q) {
+        const std::int64_t b0 = o_ext * q / parts, b1 = o_ext * (q + 1) / parts;
+        tcb_gemm_desc d = desc_of(*recipe(e, b1 - b0));
+        d.beta = beta;
+        check(tcb_gemm(&d, dl_ + e0 * sa + b0 * o_sa, dr_ + e0 * sb + b0 * o_sb,
+                       do_ + b0 * o_sc),
+              "contraction");
+        void* block_done = h.event();
+        check(tcb_event_record(block_done, compute), "event");
+        check(tcb_stream_wait_event(h.down, block_done), "event");
+        check(tcb_memcpy_async(out + b0 * o_sc, do_ + b0 * o_sc, (b1 - b0) * o_sc * 8, h.down),
+              "download");
+      }
+    }
     e0 += e;
   }
-  void* done = h.event();
-  check(tcb_event_record(done, compute), "event");
-  check(tcb_stream_wait_event(h.down, done), "event");
-  check(tcb_memcpy_async(out, do_, no_ * 8, h.down), "download");
+  if (parts < 2) {
+    void* done = h.event();
+    check(tcb_event_record(done, compute), "event");
+    check(tcb_stream_wait_event(h.down, done), "event");
+    check(tcb_memcpy_async(out, do_, no_ * 8, h.down), "download");
+  }
   h.finish(compute, wait, set_);
   launches_ = tcb_launch_count() - before;
   return slabs;
