@@ -352,7 +352,10 @@ struct B200Options {
 /// recognises it and lowers a whole plan to device launches instead.
 std::unique_ptr<KernelBackend> make_b200_backend(const B200Options& options = {});
 
-/// "b200" (also "device") -> make_b200_backend(). The reference names
+/// "b200" (also "device") -> make_b200_backend(); "b200-sliced" -> the same
+/// device BLAS calls driven slice by slice through the plan's loop nest (the
+/// reference's execution structure: one device call per slice, operands
+/// copied per call), for comparing forced kernels. The reference names
 /// "reference" and "external" are CPU backends and are not part of this
 /// engine: they throw std::invalid_argument naming the replacement.
 std::unique_ptr<KernelBackend> make_backend(const std::string& name);
@@ -614,6 +617,12 @@ struct BenchRow {
   std::int64_t packed_bytes = 0;
   bool available = false;
   bool verified_ok = true;  // true when sampling is off or the sample matched
+  /// What ran (not in the reference): with backend "b200" every forced-kernel
+  /// row executes the contraction's own device recipe (one launch, e.g.
+  /// "L1 gemm"), so rows of one contraction differ only in planning; with
+  /// "b200-sliced" the forced plan's loop nest ran slice by slice
+  /// ("sliced GER" ...). write_bench_csv appends it as an `executed` column.
+  std::string executed;
 };
 
 std::vector<BenchRow> run_bench(const BenchConfig& config);

@@ -144,6 +144,40 @@ std::unique_ptr<KernelBackend> make_b200_backend(const B200Options& options) {
   return std::make_unique<B200Backend>(options);
 }
 
+namespace {
+// The B200 backend's BLAS calls behind a type execute() does not lower:
+// plans run slice by slice, one device call per slice (execute_sliced).
+class SlicedB200 final : public KernelBackend {
+ public:
+  SlicedB200() : dev_(B200Options{}) {}
+  const std::string& name() const override {
+    static const std::string n = "b200-sliced";
+    return n;
+  }
+  void gemm(bool ta, bool tb, std::int64_t m, std::int64_t n, std::int64_t k, double alpha,
+            const double* a, std::int64_t lda, const double* b, std::int64_t ldb, double beta,
+            double* c, std::int64_t ldc) const override {
+    dev_.gemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+  }
+  void gemv(bool trans, std::int64_t m, std::int64_t n, double alpha, const double* a,
+            std::int64_t lda, const double* x, std::int64_t incx, double beta, double* y,
+            std::int64_t incy) const override {
+    dev_.gemv(trans, m, n, alpha, a, lda, x, incx, beta, y, incy);
+  }
+  void ger(std::int64_t m, std::int64_t n, double alpha, const double* x, std::int64_t incx,
+           const double* y, std::int64_t incy, double* a, std::int64_t lda) const override {
+    dev_.ger(m, n, alpha, x, incx, y, incy, a, lda);
+  }
+  double dot(std::int64_t k, const double* x, std::int64_t incx, const double* y,
+             std::int64_t incy) const override {
+    return dev_.dot(k, x, incx, y, incy);
+  }
+
+ private:
+  B200Backend dev_;
+};
+}  // namespace
+
 std::unique_ptr<KernelBackend> make_reference_backend() {
   throw std::invalid_argument(
       "make_reference_backend: the reference's CPU backend is not part of this engine, which "
@@ -158,6 +192,7 @@ std::unique_ptr<KernelBackend> make_eigen_backend() {
 
 std::unique_ptr<KernelBackend> make_backend(const std::string& name) {
   if (name == "b200" || name == "device") return make_b200_backend();
+  if (name == "b200-sliced") return std::make_unique<SlicedB200>();
   if (name == "reference" || name == "external")
     throw std::invalid_argument("backend '" + name +
                                 "' is a CPU backend of the reference engine; this engine runs on "

@@ -16,8 +16,9 @@ COLS = ["experiment", "expression", "size", "kernel", "backend", "repetitions",
 
 def rows(text):
     r = list(csv.reader(io.StringIO(text)))
-    assert r[0] == COLS
-    return [dict(zip(COLS, x)) for x in r[1:]]
+    # the reference's columns, then `executed` (what the device ran)
+    assert r[0] == COLS + ["executed"]
+    return [dict(zip(COLS + ["executed"], x)) for x in r[1:]]
 
 
 def test_square3d_rows_verify_and_report(dev):
@@ -67,3 +68,22 @@ def test_execute_loop_with_pinned_recycled_blocks(dev):
         text, ok = T.bench_csv("custom", sizes=(1,), kernels=("GEMM",), repetitions=4,
                                verify=True, custom_expr=e, custom_extents=x)
         assert ok, (e, x, text)
+
+
+def test_forced_kernels_are_marked_and_sliced_backend_runs_them(dev):
+    # b200: every forced kernel runs the contraction's device recipe, marked
+    text, ok = T.bench_csv("square3d", sizes=(24,), kernels=("GEMM", "GER", "DOT"),
+                           repetitions=2, verify=True)
+    assert ok
+    for r in rows(text):
+        if r["median_seconds"] != "NA":
+            assert r["executed"].startswith(("L1", "L2", "L3", "L4")), r
+    # b200-sliced: the forced plan's loop nest, one device call per slice
+    text, ok = T.bench_csv("square3d", sizes=(12,), kernels=("GEMM", "GER", "DOT"),
+                           backend="b200-sliced", repetitions=1, verify=True)
+    assert ok
+    rs = rows(text)
+    for r in rs:
+        if r["median_seconds"] != "NA":
+            assert r["executed"] == "sliced " + r["kernel"], r
+            assert r["backend"] == "b200-sliced"
