@@ -139,6 +139,17 @@ typedef struct tcb_gemm_info {
 } tcb_gemm_info;
 
 int tcb_gemm(const tcb_gemm_desc* d, const double* A, const double* B, double* C);
+/* tcb_gemm whose operand reads wait, on the device, until the 64-bit word at
+ * `gate` (device memory) is >= value — set from another stream with
+ * tcb_stream_write_value after that stream's uploads. The calling stream sees
+ * no host-visible wait, so back-to-back GEMMs keep programmatic dependent
+ * launch. TCB_EUNSUPPORTED where the device lacks 64-bit stream memory
+ * operations. */
+int tcb_gemm_gated(const tcb_gemm_desc* d, const double* A, const double* B, double* C,
+                   const uint64_t* gate, uint64_t value);
+/* Stream-ordered write of `value` to device word `addr` once the stream's
+ * earlier work (and its memory writes) completed (cuStreamWriteValue64). */
+int tcb_stream_write_value(void* stream, uint64_t* addr, uint64_t value);
 int tcb_last_gemm_info(tcb_gemm_info* info);
 /* TCB_OK when tcb_gemm can execute `d` for 16-byte aligned operands (only
  * descriptors with index groups can be refused: the groups must map onto the

@@ -63,6 +63,55 @@ int ensure_init() {
 
 }  // namespace tcb
 
+namespace tcb {
+namespace {
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned);
+struct MemOps {
+  WriteValueFn write = nullptr, wait = nullptr;
+};
+const MemOps& mem_ops() {
+  static MemOps ops = [] {
+    MemOps o;
+    int dev = 0, ok = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ok, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS),
+                           dev);
+    if (!ok) return o;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      o.write = reinterpret_cast<WriteValueFn>(f);
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      o.wait = reinterpret_cast<WriteValueFn>(f);
+    return o;
+  }();
+  return ops;
+}
+}  // namespace
+
+int stream_write_value(cudaStream_t s, uint64_t* addr, uint64_t value) {
+  const MemOps& o = mem_ops();
+  if (!o.write) return set_error(TCB_EUNSUPPORTED, "64-bit stream memory operations unavailable");
+  // default flags: a memory barrier orders the stream's earlier copies first
+  const CUresult r = o.write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
+                             value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return set_error(TCB_ECUDA, "cuStreamWriteValue64 failed");
+  return TCB_OK;
+}
+
+int stream_wait_value(cudaStream_t s, const uint64_t* addr, uint64_t value) {
+  const MemOps& o = mem_ops();
+  if (!o.wait) return set_error(TCB_EUNSUPPORTED, "64-bit stream memory operations unavailable");
+  const CUresult r = o.wait(reinterpret_cast<CUstream>(s),
+                            reinterpret_cast<CUdeviceptr>(const_cast<uint64_t*>(addr)), value,
+                            CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return set_error(TCB_ECUDA, "cuStreamWaitValue64 failed");
+  return TCB_OK;
+}
+}  // namespace tcb
+
 using namespace tcb;
 
 #define TCB_TRY_INIT()              \
@@ -453,6 +502,39 @@ int tcb_gemm(const tcb_gemm_desc* d, const double* A, const double* B, double* C
   }
   if (d->n == 1 || d->m == 1) return launch_gemv(*d, A, B, C);
   return launch_gemm(*d, A, B, C);
+}
+
+int tcb_stream_write_value(void* stream, uint64_t* addr, uint64_t value) {
+  TCB_TRY_INIT();
+  if (!addr) return set_error(TCB_EINVAL, "tcb_stream_write_value: null address");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : state().stream;
+  note_stream_op(s);
+  return stream_write_value(s, addr, value);
+}
+
+int tcb_gemm_gated(const tcb_gemm_desc* d, const double* A, const double* B, double* C,
+                   const uint64_t* gate, uint64_t value) {
+  TCB_TRY_INIT();
+  if (!gate) return tcb_gemm(d, A, B, C);
+  int rc = check_desc(d);
+  if (rc != TCB_OK) return rc;
+  ThreadState& st = state();
+  int64_t batch = 1;
+  for (int i = 0; i < d->nbatch; ++i) batch *= d->bat_ext[i];
+  const bool dmma = !(d->m == 0 || d->n == 0 || batch == 0 || d->alpha == 0.0 || d->k == 0 ||
+                      d->n == 1 || d->m == 1);
+  if (!dmma) {  // paths without a device-side gate: wait in the stream
+    note_stream_op();
+    rc = stream_wait_value(st.stream, gate, value);
+    if (rc != TCB_OK) return rc;
+    return tcb_gemm(d, A, B, C);
+  }
+  st.last_info = tcb_gemm_info{};
+  st.gate = reinterpret_cast<const unsigned long long*>(gate);
+  st.gate_value = value;
+  rc = launch_gemm(*d, A, B, C);
+  st.gate = nullptr;
+  return rc;
 }
 
 int tcb_last_gemm_info(tcb_gemm_info* info) {

@@ -144,6 +144,12 @@ struct Params {
   unsigned long long pace_base;
   int pace_shift, pace_slack, pace_grid;
   unsigned pace_total;
+  // gate (tcb_gemm_gated): the producer issues no operand load before
+  // *gate >= gate_value — a device-side dependency on an upload stream
+  // (tcb_stream_write_value), so consecutive GEMMs keep programmatic
+  // dependent launch instead of a host-visible stream wait between them
+  const unsigned long long* gate;
+  unsigned long long gate_value;
   // whole tiles of odd waves issue their k-blocks in descending order: the
   // k-slices a wave used last are the next wave's first, still in L2 (the
   // consumers are order-agnostic; the tile's sum order is fixed per tile)
@@ -390,6 +396,18 @@ __device__ __forceinline__ int sk_owner(const Params& p, int pos) {
     else hi = mid - 1;
   }
   return lo;
+}
+
+// Wait for the gate (see Params), then order the async-proxy (TMA) operand
+// reads after the acquire.
+__device__ __forceinline__ void gate_wait(const Params& p) {
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.gate) : "memory");
+    if (v >= p.gate_value) break;
+    __nanosleep(256);
+  }
+  asm volatile("fence.proxy.async;" ::: "memory");
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -702,6 +720,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     // ============================ producer ============================
     if (USE_TMA && tid != 0) return;
+    if (p.gate != nullptr) gate_wait(p);
     LoadIter<SPLITK> li;
     li.template start<USE_TMA>(p);
     uint32_t g = 0;
@@ -1457,6 +1476,8 @@ bool make_pace_ready(ThreadState& st) {
 int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C) {
   ThreadState& st = state();
   Params p{};
+  p.gate = st.gate;  // set by tcb_gemm_gated for this launch only
+  p.gate_value = st.gate_value;
   p.A = A;
   p.B = B;
   p.C = C;

@@ -27,6 +27,8 @@ struct ThreadState {
   int last_splits = 0;             // (G, tiles, kblocks) of the last stream-K launch
   int64_t last_tiles = 0;
   int64_t last_kblocks = 0;
+  const unsigned long long* gate = nullptr;  // tcb_gemm_gated: the next launch's gate
+  unsigned long long gate_value = 0;
   unsigned long long* pace = nullptr;  // k-pacing counter (monotonic across launches)
   unsigned long long pace_base = 0;    // its value once every earlier launch has finished
   bool pace_reset = true;              // re-zero before the next paced launch
@@ -81,5 +83,9 @@ int launch_permute(int rank, const int64_t* ext, const int64_t* src_str, const d
 int launch_gemv(const tcb_gemm_desc& d, const double* A, const double* B, double* C);
 int launch_scale(const tcb_gemm_desc& d, double* C);
 int num_sms();
+// cuStreamWriteValue64 / cuStreamWaitValue64 (driver entry points; null when
+// the driver lacks them or the device cannot do 64-bit stream memory ops)
+int stream_write_value(cudaStream_t s, uint64_t* addr, uint64_t value);
+int stream_wait_value(cudaStream_t s, const uint64_t* addr, uint64_t value);
 
 }  // namespace tcb

@@ -338,9 +338,21 @@ struct PreparedContraction::Pipes {
   void* compute_done[2] = {nullptr, nullptr};
   void* down_done[2] = {nullptr, nullptr};
   bool pending[2] = {false, false};
+  // device word the upload stream advances after each slab's copies
+  // (tcb_stream_write_value); slab GEMMs wait for it on the device
+  // (tcb_gemm_gated), so the compute stream holds only GEMMs and consecutive
+  // slab GEMMs overlap under programmatic dependent launch
+  std::uint64_t* gate = nullptr;
+  std::uint64_t gate_epoch = 0;
+  bool gate_ok = true;
   Pipes() {
     check(tcb_stream_create(&up), "stream");
     check(tcb_stream_create(&down), "stream");
+    void* g = nullptr;
+    if (tcb_alloc(&g, 8) == TCB_OK && tcb_memset0(g, 8) == TCB_OK && tcb_sync() == TCB_OK)
+      gate = static_cast<std::uint64_t*>(g);
+    else
+      gate_ok = false;
     for (int i = 0; i < 2; ++i) {
       check(tcb_event_create(&compute_done[i]), "event");
       check(tcb_event_create(&down_done[i]), "event");
@@ -348,6 +360,8 @@ struct PreparedContraction::Pipes {
   }
   ~Pipes() {
     if (down) tcb_stream_sync(down);
+    if (up) tcb_stream_sync(up);
+    tcb_free(gate);
     for (void* e : events) tcb_event_destroy(e);
     for (int i = 0; i < 2; ++i) {
       if (compute_done[i]) tcb_event_destroy(compute_done[i]);
@@ -1020,15 +1034,22 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   if (!auto_slabs) {
     for (int i = 0; i < slabs; ++i) sizes.push_back(E / slabs + (i < E % slabs ? 1 : 0));
   } else {
+    // Nominal slabs are an eighth of the label: long slab GEMMs run at the
+    // whole contraction's efficiency (cfg5: 2048 k-blocks per tile, the
+    // stream-K tail applies; 64 slabs of 256 k-blocks lost 3 % to per-slab
+    // wave tails and epilogues). The ramp grows by 1.5x per slab so each
+    // upload (PCIe, ~55 GB/s) stays shorter than the previous slab's
+    // contraction.
     const std::int64_t unit = ((sa | sb) & 1) ? 2 : 1;
-    const std::int64_t nominal = std::max<std::int64_t>(unit, E / slabs / unit * unit);
+    const std::int64_t nominal = std::max<std::int64_t>(unit, (E + 7) / 8 / unit * unit);
     std::int64_t rest = E, ramp = unit;
     while (rest > 0) {
-      std::int64_t e = std::min({rest, ramp, nominal});
+      std::int64_t e = std::min({rest, ramp / unit * unit, nominal});
+      e = std::max(e, std::min(rest, unit));
       if (rest - e > 0 && rest - e < (nominal + 1) / 2) e = rest;
       sizes.push_back(e);
       rest -= e;
-      ramp *= 2;
+      ramp = std::max(ramp + unit, ramp * 3 / 2);
     }
     slabs = static_cast<int>(sizes.size());
   }
@@ -1091,22 +1112,32 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     check(tcb_memcpy2d_async(dr_ + e0 * sb, sb * E * 8, right + e0 * sb, sb * E * 8, sb * e * 8,
                              hb, h.up),
           "upload");
-    void* ready = h.event();
-    check(tcb_event_record(ready, h.up), "event");
-    check(tcb_stream_wait_event(compute, ready), "event");
+    // the slab's contraction waits for its uploads: on the device through the
+    // gate where available, else through an event on the compute stream
+    bool gated = h.gate_ok && tcb_stream_write_value(h.up, h.gate, h.gate_epoch + 1) == TCB_OK;
+    if (gated) {
+      ++h.gate_epoch;
+    } else {
+      h.gate_ok = false;
+      void* ready = h.event();
+      check(tcb_event_record(ready, h.up), "event");
+      check(tcb_stream_wait_event(compute, ready), "event");
+    }
+    auto gemm = [&](const tcb_gemm_desc& d, const double* a, const double* b, double* c) {
+      check(gated ? tcb_gemm_gated(&d, a, b, c, h.gate, h.gate_epoch) : tcb_gemm(&d, a, b, c),
+            "contraction");
+    };
     const double beta = s == 0 ? 0.0 : 1.0;
     if (s + 1 < slabs || parts < 2) {
       tcb_gemm_desc d = desc_of(*recipe(e, 0));
       d.beta = beta;
-      check(tcb_gemm(&d, dl_ + e0 * sa, dr_ + e0 * sb, do_), "contraction");
+      gemm(d, dl_ + e0 * sa, dr_ + e0 * sb, do_);
     } else {
       for (int q = 0; q < parts; ++q) {
         const std::int64_t b0 = o_ext * q / parts, b1 = o_ext * (q + 1) / parts;
         tcb_gemm_desc d = desc_of(*recipe(e, b1 - b0));
         d.beta = beta;
-        check(tcb_gemm(&d, dl_ + e0 * sa + b0 * o_sa, dr_ + e0 * sb + b0 * o_sb,
-                       do_ + b0 * o_sc),
-              "contraction");
+        gemm(d, dl_ + e0 * sa + b0 * o_sa, dr_ + e0 * sb + b0 * o_sb, do_ + b0 * o_sc);
         void* block_done = h.event();
         check(tcb_event_record(block_done, compute), "event");
         check(tcb_stream_wait_event(h.down, block_done), "event");

@@ -78,6 +78,8 @@ TCB_API = {
     "tcb_host_is_pinned": (i32, [vp, C.POINTER(C.c_int)]),
     "tcb_gemm": (i32, [C.POINTER(GemmDesc), vp, vp, vp]),
     "tcb_gemm_check": (i32, [C.POINTER(GemmDesc)]),
+    "tcb_gemm_gated": (i32, [C.POINTER(GemmDesc), vp, vp, vp, vp, C.c_uint64]),
+    "tcb_stream_write_value": (i32, [vp, vp, C.c_uint64]),
     "tcb_last_gemm_info": (i32, [C.POINTER(GemmInfo)]),
     "tcb_dgemm": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64]),
     "tcb_dgemm_strided_batched": (i32, [i32, i32, i64, i64, i64, f64, vp, i64, i64, vp, i64,

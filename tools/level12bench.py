@@ -1,7 +1,7 @@
 """k4 (GEMV / DOT) HBM roofline: reference class-2 and class-1 contractions
 large enough to be HBM-bound, through the prepared plan-level API. Prints one
 JSON line per case: algorithmic bytes = every operand element read once +
-the result written, vs the measured 6465 GB/s copy bandwidth."""
+the result written, vs the measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs, 6552 GB/s)."""
 import json
 import sys
 from pathlib import Path
@@ -10,7 +10,19 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import ctypes as C
 import paper_1307_2100_b200 as T
 
-HBM = 6465.2
+def _hbm_peak() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth of this pool's
+    B200s), else the B200_PROFILING.md fallback."""
+    import json
+    from pathlib import Path
+    f = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(f.read_text())["hbm_gbs"])
+    except Exception:
+        return 6552.0
+
+
+HBM = _hbm_peak()
 dev = T.native.device()
 T.check(dev.tcb_init(0))
 CASES = [

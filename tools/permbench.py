@@ -13,7 +13,19 @@ import paper_1307_2100_b200 as T
 
 dev = T.native.device()
 T.check(dev.tcb_init(0))
-HBM = 6465.2
+def _hbm_peak() -> float:
+    """MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth of this pool's
+    B200s), else the B200_PROFILING.md fallback."""
+    import json
+    from pathlib import Path
+    f = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(f.read_text())["hbm_gbs"])
+    except Exception:
+        return 6552.0
+
+
+HBM = _hbm_peak()
 
 
 def perm_case(name, ext, src_str, reps=20):
