@@ -401,6 +401,34 @@ def golden_parity(cfg: str, expr: str, full: str, label: str | None, lo: int, hi
     return res
 
 
+def peer_self_test(T, dev, prep, exchange, scat, block, world, rank, torch, backend):
+    """One host-synchronised step of the fused K-split exchange, checked
+    against a plain all-reduce of the ranks' partial outputs (torch.distributed).
+    Returns None when the rank's block agrees (rel. error <= 1e-12), else why."""
+    import ctypes as C
+    saved = exchange.host_sync
+    exchange.host_sync = True
+    try:
+        exchange.step(prep, scat.ptr)
+    finally:
+        exchange.host_sync = saved
+    T.check(dev.tcb_sync(), "tcb_sync")
+    got = np.empty(block)
+    T.check(dev.tcb_d2h(got.ctypes.data, scat.ptr, block * 8), "tcb_d2h")
+    prep.run()  # the rank's partial C, unscattered
+    prep.sync()
+    _, _, optr = prep.device_ptrs()
+    part = np.empty(block * world)
+    T.check(dev.tcb_d2h(part.ctypes.data, optr, part.nbytes), "tcb_d2h")
+    t = torch.from_numpy(part)
+    if backend == "nccl":
+        t = t.cuda()
+    torch.distributed.all_reduce(t)
+    want = t[rank * block:(rank + 1) * block].cpu().numpy()
+    err = float(np.abs(got - want).max() / max(1.0, float(np.abs(want).max())))
+    return None if err <= 1e-12 else f"block differs from the all-reduce by {err:.3g}"
+
+
 def relaunch(args) -> int:
     """--gpus N without torchrun: spawn N ranks on this node."""
     import socket
@@ -529,18 +557,42 @@ def main() -> int:
     t_gen = time.time() - t_gen
 
     collective = exchange = None
+    exchange_note = None
     block = info["output"]
+    prep.upload(L, R)
+    if mode == "ksplit":
+        block = info["output"] // world
+        scat = T.DeviceBuffer(block * 8)
     if mode == "ksplit" and args.exchange == "peer":
         # fused: the GEMM epilogue writes each block of this rank's partial C
         # into its owner's receive buffer through the peer window (tcb_peer_*),
-        # then each rank sums its received slots (partition.PeerKSplit)
-        block = info["output"] // world
-        scat = T.DeviceBuffer(block * 8)
-        # ranks sharing one GPU (gloo plumbing runs): host barriers between the
-        # phases instead of device-side flag waits across processes
-        exchange = P.PeerKSplit(dev, world, rank, block, torch.distributed,
-                                host_sync=backend != "nccl")
-    elif mode == "ksplit":
+        # then each rank sums its received slots (partition.PeerKSplit).
+        # Ranks sharing one GPU (gloo plumbing runs): host barriers between the
+        # phases instead of device-side flag waits across processes.
+        # Self-test first (one host-synchronised step against a plain
+        # all-reduce of the partials); any failure falls back to NCCL.
+        why = None
+        try:
+            exchange = P.PeerKSplit(dev, world, rank, block, torch.distributed,
+                                    host_sync=backend != "nccl")
+            why = peer_self_test(T, dev, prep, exchange, scat, block, world, rank, torch,
+                                 backend)
+        except Exception as e:  # noqa: BLE001 - any failure selects the fallback
+            why = f"{type(e).__name__}: {e}"
+        failed = torch.tensor([1.0 if why else 0.0], dtype=torch.float64,
+                              device="cuda" if backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(failed, op=torch.distributed.ReduceOp.MAX)
+        if failed.item() > 0:
+            if exchange is not None:
+                try:
+                    exchange.close()
+                except Exception:
+                    pass
+            exchange = None
+            exchange_note = f"peer exchange self-test failed ({why or 'on another rank'}); NCCL"
+            if backend != "nccl":
+                raise SystemExit(exchange_note)
+    if mode == "ksplit" and exchange is None:
         if backend != "nccl":
             raise SystemExit("ksplit (cfg5) with --exchange nccl needs the nccl backend")
         # the engine's own NCCL communicator (tcb_comm_*, include/tcb.h); the
@@ -558,12 +610,9 @@ def main() -> int:
         comm = C.c_void_p()
         T.check(dev.tcb_comm_init(world, rank, uid, C.byref(comm)), "tcb_comm_init")
         _, _, optr = prep.device_ptrs()
-        block = info["output"] // world
-        scat = T.DeviceBuffer(block * 8)
 
         def collective():
             T.check(dev.tcb_reduce_scatter(optr, scat.ptr, block, comm), "tcb_reduce_scatter")
-    prep.upload(L, R)
 
     def barrier():
         if world > 1:
@@ -754,6 +803,7 @@ def main() -> int:
                              if exchange is not None else
                              "by NCCL after the GEMM (NCCL_ALGO/NCCL_PROTO pinned)")}[mode],
             "rank_extents": extents,
+            **({"exchange_fallback": exchange_note} if exchange_note else {}),
             "l2": ("inputs larger than L2 per step (A+B+C = %.0f MB > 126 MB), steps back to "
                    "back" % (ws_bytes / 2**20)) if not small else
                   ("A+B+C = %.0f MB fit in L2: L2 flushed before every step (252 MB memset "

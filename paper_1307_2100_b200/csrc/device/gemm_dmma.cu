@@ -402,10 +402,12 @@ __device__ __forceinline__ int sk_owner(const Params& p, int pos) {
 // reads after the acquire.
 __device__ __forceinline__ void gate_wait(const Params& p) {
   unsigned long long v;
+  const unsigned long long t0 = wait_clock_ns();
   for (;;) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.gate) : "memory");
     if (v >= p.gate_value) break;
     __nanosleep(256);
+    if (wait_clock_ns() - t0 > kWaitTrapNs) __trap();  // the gate was never opened
   }
   asm volatile("fence.proxy.async;" ::: "memory");
 }
@@ -981,10 +983,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (ctid == 0) {
         const unsigned target = (p.epoch + 1u) * static_cast<unsigned>(S);
         unsigned seen;
+        unsigned long long t_start = 0;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.counters + t)
                        : "memory");
-          if (seen < target) __nanosleep(32);
+          if (seen < target) {
+            __nanosleep(32);
+            const unsigned long long now = wait_clock_ns();
+            if (t_start == 0) t_start = now;
+            else if (now - t_start > kWaitTrapNs) __trap();  // a contributor never arrived
+          }
         } while (seen < target);
       }
       consumer_sync();
@@ -1722,8 +1730,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
   const auto [alo, ahi] = operand_range(d, A, true);
   const auto [blo, bhi] = operand_range(d, B, false);
   const bool pdl = !no_pdl && st.pdl_ok && st.stream == st.own_stream &&
-                   (ahi <= st.pdl_lo || alo >= st.pdl_hi) &&
-                   (bhi <= st.pdl_lo || blo >= st.pdl_hi);
+                   st.pdl_clear(alo, ahi) && st.pdl_clear(blo, bhi);
   // TCB_TRACE=<file>: append per-CTA phase timestamps of this launch (diagnostics)
   static const char* trace_path = getenv("TCB_TRACE");
   unsigned long long* trace = nullptr;
@@ -1758,8 +1765,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     // outputs of the PDL chain: a fully serialized launch starts a new chain
     // (everything before it has completed); a PDL launch extends it
     const auto [clo, chi] = output_range(d, C);
-    st.pdl_lo = pdl ? std::min(st.pdl_lo, clo) : clo;
-    st.pdl_hi = pdl ? std::max(st.pdl_hi, chi) : chi;
+    st.pdl_add(clo, chi, pdl);
     st.pdl_ok = true;
   }
   if (trace) {

@@ -156,7 +156,11 @@ __global__ void __launch_bounds__(256) peer_reduce_kernel(
     double* __restrict__ out, const unsigned long long* flags, unsigned long long epoch) {
   if (threadIdx.x < world) {
     const unsigned long long* f = flags + threadIdx.x;
-    while (ld_acquire_sys(f) < epoch) __nanosleep(256);
+    const unsigned long long t0 = wait_clock_ns();
+    while (ld_acquire_sys(f) < epoch) {
+      __nanosleep(256);
+      if (wait_clock_ns() - t0 > kWaitTrapNs) __trap();  // a peer rank never signalled
+    }
   }
   __syncthreads();
   const double2* src = reinterpret_cast<const double2*>(slots);

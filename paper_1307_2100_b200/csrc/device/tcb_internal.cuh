@@ -37,13 +37,45 @@ struct ThreadState {
   int64_t launches = 0;
   // Programmatic dependent launch: true while the operations enqueued on the
   // thread's own stream since the last fully serialized launch are all DMMA
-  // GEMMs (a PDL chain). [pdl_lo, pdl_hi) covers the union of their outputs:
-  // a GEMM launched with PDL may issue its operand loads while ANY earlier
-  // GEMM of the chain still runs (each one lets its dependent start once its
-  // own CTAs are resident), so its operands must avoid every output of the
-  // chain, not just the last one. Every other stream operation clears it.
+  // GEMMs (a PDL chain). The intervals [pdl_lo[i], pdl_hi[i]) cover the
+  // union of their outputs: a GEMM launched with PDL may issue its operand
+  // loads while ANY earlier GEMM of the chain still runs (each one lets its
+  // dependent start once its own CTAs are resident), so its operands must
+  // avoid every output of the chain, not just the last one. Up to 8 disjoint
+  // intervals are kept (repeated calls rotating over several output buffers
+  // stay chained); beyond that they collapse into one bounding interval.
+  // Every other stream operation clears the chain.
+  static constexpr int kPdlRanges = 8;
   bool pdl_ok = false;
-  uintptr_t pdl_lo = 0, pdl_hi = 0;
+  int pdl_n = 0;
+  uintptr_t pdl_lo[kPdlRanges] = {}, pdl_hi[kPdlRanges] = {};
+  bool pdl_clear(uintptr_t lo, uintptr_t hi) const {  // [lo, hi) misses every chain output
+    for (int i = 0; i < pdl_n; ++i)
+      if (lo < pdl_hi[i] && pdl_lo[i] < hi) return false;
+    return true;
+  }
+  void pdl_add(uintptr_t lo, uintptr_t hi, bool extend) {
+    if (!extend) pdl_n = 0;
+    for (int i = 0; i < pdl_n; ++i)
+      if (lo <= pdl_hi[i] && pdl_lo[i] <= hi) {  // overlapping or adjacent: merge
+        pdl_lo[i] = lo < pdl_lo[i] ? lo : pdl_lo[i];
+        pdl_hi[i] = hi > pdl_hi[i] ? hi : pdl_hi[i];
+        return;
+      }
+    if (pdl_n == kPdlRanges) {  // collapse into one bounding interval
+      for (int i = 1; i < pdl_n; ++i) {
+        pdl_lo[0] = pdl_lo[i] < pdl_lo[0] ? pdl_lo[i] : pdl_lo[0];
+        pdl_hi[0] = pdl_hi[i] > pdl_hi[0] ? pdl_hi[i] : pdl_hi[0];
+      }
+      pdl_n = 1;
+      pdl_lo[0] = lo < pdl_lo[0] ? lo : pdl_lo[0];
+      pdl_hi[0] = hi > pdl_hi[0] ? hi : pdl_hi[0];
+      return;
+    }
+    pdl_lo[pdl_n] = lo;
+    pdl_hi[pdl_n] = hi;
+    ++pdl_n;
+  }
   tcb_gemm_info last_info{};
 };
 
@@ -73,6 +105,18 @@ inline void note_stream_op(cudaStream_t stream = nullptr) {
   ThreadState& st = state();
   if (stream == nullptr || stream == st.stream) st.pdl_ok = false;
 }
+
+// Device-side waits on another grid, process or stream give up after this
+// long and trap (the kernel fails with an error instead of hanging the GPU):
+// a peer rank that died, an upload that never came.
+#ifdef __CUDACC__
+constexpr unsigned long long kWaitTrapNs = 60ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long wait_clock_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 // Device-side launchers (implemented in the .cu files).
 int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double* C);
