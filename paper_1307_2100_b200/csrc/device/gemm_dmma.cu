@@ -117,6 +117,15 @@ struct Params {
   int dp_tiles;
   int64_t work;
   int sk_start[SK_MAX + 1];
+  // reduction assignment (host-built): CTA c sums pairs [red_p0, red_p1) of
+  // tile red_tile (absolute index, -1 = none) in slot j = 0, 1. A CTA whose
+  // share crosses a tile boundary reduces in one of its two tiles only (the
+  // one where it computed more), with a pair range in proportion to its
+  // whole share, so no CTA waits for and sums two tiles (those CTAs ended
+  // the launch 3-4 us after the others on cfg1).
+  int red_tile[2][SK_MAX];
+  int red_p0[2][SK_MAX];
+  int red_p1[2][SK_MAX];
   double* ws;
   unsigned* counters;
   unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
@@ -834,7 +843,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   trace_mark(p, 0, tl);
   SegIter<SPLITK> segs;
   segs.init(p);
-  int64_t seg_tile0 = -1, seg_tile1 = -1;  // stream-K: tiles of this CTA's partial segments
   int npart = 0;
   int64_t u;
   int kb0, kb1;
@@ -971,7 +979,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (npart == 0) trace_mark(p, 3, tl);
       if (ctid == 0)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + u) : "memory");
-      (npart == 0 ? seg_tile0 : seg_tile1) = u;
       ++npart;
       continue;
     }
@@ -1003,7 +1010,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool use_beta = p.beta != 0.0;
 #pragma unroll 1
     for (int j = 0; j < 2; ++j) {
-      const int64_t t = j == 0 ? seg_tile0 : seg_tile1;
+      const int64_t t = p.red_tile[j][blockIdx.x];
       if (t < 0) break;
       const int tk0 = static_cast<int>(t * p.kblocks);
       const int first = sk_owner(p, tk0);
@@ -1051,10 +1058,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       consumer_sync();
       if (j == 0) trace_mark(p, 4, tl);
       const double2* ws = reinterpret_cast<const double2*>(p.ws);
-      const int lo = max(p.sk_start[blockIdx.x], tk0) - tk0;
-      const int hi = min(p.sk_start[blockIdx.x + 1], tk0 + p.kblocks) - tk0;
-      const int p0 = static_cast<int>(static_cast<int64_t>(PAIRS) * lo / p.kblocks);
-      const int p1 = static_cast<int>(static_cast<int64_t>(PAIRS) * hi / p.kblocks);
+      const int p0 = p.red_p0[j][blockIdx.x];
+      const int p1 = p.red_p1[j][blockIdx.x];
       // Each thread owns up to RED pairs of the slice and issues 4 partial
       // loads per pair before summing (few L2 round trips, not S).
       constexpr int RED = 4;
@@ -1679,6 +1684,66 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       if (p.sk_start[c + 1] > p.sk_start[c] &&
           (p.sk_start[c + 1] - 1) / kblocks - p.sk_start[c] / kblocks > 1)
         return set_error(TCB_EUNSUPPORTED, "gemm: stream-K share spans more than two tiles");
+    // reduction assignment (see Params::red_tile)
+    {
+      constexpr int64_t PAIRS = BM * BN / 2;
+      for (int j = 0; j < 2; ++j)
+        for (int c = 0; c < SK_MAX; ++c) {
+          p.red_tile[j][c] = -1;
+          p.red_p0[j][c] = p.red_p1[j][c] = 0;
+        }
+      auto w_of = [&](int c, int64_t t) {  // k-blocks of CTA c's share in tile t
+        const int64_t lo = std::max<int64_t>(p.sk_start[c], t * kblocks);
+        const int64_t hi = std::min<int64_t>(p.sk_start[c + 1], (t + 1) * kblocks);
+        return std::max<int64_t>(0, hi - lo);
+      };
+      auto tiles_of = [&](int c, int64_t& t0, int64_t& t1) {  // t1 = -1: one tile
+        t0 = t1 = -1;
+        if (p.sk_start[c + 1] <= p.sk_start[c]) return;
+        t0 = p.sk_start[c] / kblocks;
+        const int64_t tl = (p.sk_start[c + 1] - 1) / kblocks;
+        if (tl != t0) t1 = tl;
+      };
+      // preferred tile of each CTA: its only tile, or the one it computed
+      // more of (the later one on a tie)
+      std::vector<int64_t> pref(G, -1);
+      for (int c = 0; c < G; ++c) {
+        int64_t t0, t1;
+        tiles_of(c, t0, t1);
+        pref[c] = t1 < 0 ? t0 : (w_of(c, t0) > w_of(c, t1) ? t0 : t1);
+      }
+      int cf = 0;  // first contributor of tile t (two-pointer sweep)
+      for (int64_t t = dp; t < tiles; ++t) {
+        while (cf + 1 < G && p.sk_start[cf + 1] <= t * kblocks) ++cf;
+        int cl = cf;
+        while (cl + 1 < G && p.sk_start[cl + 1] <= (t + 1) * kblocks - 1) ++cl;
+        // reducers: contributors preferring t; else the largest contributor
+        std::vector<std::pair<int, int64_t>> red;  // (CTA, weight)
+        for (int c = cf; c <= cl; ++c) {
+          if (w_of(c, t) == 0 || pref[c] != t) continue;
+          red.emplace_back(c, p.sk_start[c + 1] - p.sk_start[c]);
+        }
+        if (red.empty()) {
+          int best = cf;
+          for (int c = cf; c <= cl; ++c)
+            if (w_of(c, t) > w_of(best, t)) best = c;
+          red.emplace_back(best, w_of(best, t));
+        }
+        int64_t W_t = 0;
+        for (const auto& r : red) W_t += r.second;
+        int64_t cum = 0;
+        for (const auto& r : red) {
+          const int c = r.first;
+          const int j = p.red_tile[0][c] < 0 ? 0 : 1;
+          if (j == 1 && p.red_tile[1][c] >= 0)
+            return set_error(TCB_EUNSUPPORTED, "gemm: stream-K reduction assignment");
+          p.red_tile[j][c] = static_cast<int>(t);
+          p.red_p0[j][c] = static_cast<int>(PAIRS * cum / W_t);
+          cum += r.second;
+          p.red_p1[j][c] = static_cast<int>(PAIRS * cum / W_t);
+        }
+      }
+    }
     // most contributors of one shared tile (reported), by a two-pointer sweep
     int c = 0;
     for (int64_t t = dp; t < tiles; ++t) {

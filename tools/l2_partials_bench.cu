@@ -13,7 +13,7 @@
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
   return t;
 }
 
@@ -102,9 +102,9 @@ int main() {
       cudaMemcpy(h.data(), tr, G * 4 * 8, cudaMemcpyDeviceToHost);
       std::vector<double> st, wt, rd;
       for (int b = 0; b < G; ++b) {
-        st.push_back((h[b * 4 + 1] - h[b * 4 + 0]) / 1e3);
-        wt.push_back((h[b * 4 + 2] - h[b * 4 + 1]) / 1e3);
-        rd.push_back((h[b * 4 + 3] - h[b * 4 + 2]) / 1e3);
+        st.push_back((h[b * 4 + 1] - h[b * 4 + 0]) / 1965.0);
+        wt.push_back((h[b * 4 + 2] - h[b * 4 + 1]) / 1965.0);
+        rd.push_back((h[b * 4 + 3] - h[b * 4 + 2]) / 1965.0);
       }
       auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
       auto mx = [](std::vector<double> v) { return *std::max_element(v.begin(), v.end()); };

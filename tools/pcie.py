@@ -40,3 +40,13 @@ both = timed(lambda: (dev.tcb_memcpy_async(d1.ptr, h1.ctypes.data, n * 8, s1),
 gb = n * 8 / 1e9
 print(json.dumps({"bytes": n * 8, "h2d_GBps": round(gb / h2d, 1), "d2h_GBps": round(gb / d2h, 1),
                   "concurrent_total_GBps": round(2 * gb / both, 1)}))
+
+# 2-D uploads (the streamed paths' slab copies): rows of w bytes out of a
+# pitch 2x wider, 64 MB per copy
+for w in (4096, 8192, 16384, 32768, 65536, 262144):
+    rows = (64 << 20) // w
+    pitch = 2 * w
+    if rows * pitch > n * 8:
+        continue
+    t = timed(lambda: dev.tcb_memcpy2d_async(d1.ptr, pitch, h1.ctypes.data, pitch, w, rows, s1))
+    print(json.dumps({"h2d_2d_row_bytes": w, "rows": rows, "GBps": round(rows * w / 1e9 / t, 1)}))
