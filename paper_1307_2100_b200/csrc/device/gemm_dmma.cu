@@ -117,15 +117,6 @@ struct Params {
   int dp_tiles;
   int64_t work;
   int sk_start[SK_MAX + 1];
-  // reduction assignment (host-built): CTA c sums pairs [red_p0, red_p1) of
-  // tile red_tile (absolute index, -1 = none) in slot j = 0, 1. A CTA whose
-  // share crosses a tile boundary reduces in one of its two tiles only (the
-  // one where it computed more), with a pair range in proportion to its
-  // whole share, so no CTA waits for and sums two tiles (those CTAs ended
-  // the launch 3-4 us after the others on cfg1).
-  int red_tile[2][SK_MAX];
-  int red_p0[2][SK_MAX];
-  int red_p1[2][SK_MAX];
   double* ws;
   unsigned* counters;
   unsigned epoch;  // split-K: counters reach (epoch+1)*splits in this launch
@@ -168,6 +159,11 @@ struct Params {
   // streamed operand evict_first, so the stream does not push the group out
   int a_hint, b_hint, c_hint;
 };
+
+// Params + three tensor maps are the kernel's parameters: stay within the
+// classic 4 KB (a 6 KB block carrying per-CTA tables indexed at run time
+// failed a batched stream-K launch; not root-caused, so not repeated)
+static_assert(sizeof(Params) + 3 * sizeof(CUtensorMap) <= 4096, "kernel parameters above 4 KB");
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -432,15 +428,70 @@ struct SegIter {
   }
 };
 
-// stream-K: the CTA whose share holds position pos (binary search of sk_start)
+// stream-K: the CTA whose share holds position pos — the last c with
+// sk_start[c] <= pos. Shares are near-equal, so a proportional guess corrected
+// by a step or two replaces a binary search (8 dependent parameter loads).
 __device__ __forceinline__ int sk_owner(const Params& p, int pos) {
-  int lo = 0, hi = p.sk_grid - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (p.sk_start[mid] <= pos) lo = mid;
-    else hi = mid - 1;
+  const int n = p.sk_grid, base = p.sk_start[0];
+  const float span = static_cast<float>(p.sk_start[n] - base);
+  int c = span > 0.f ? static_cast<int>(static_cast<float>(pos - base) * n / span) : 0;
+  c = min(max(c, 0), n - 1);
+  while (c > 0 && p.sk_start[c] > pos) --c;
+  while (c + 1 < n && p.sk_start[c + 1] <= pos) ++c;
+  return c;
+}
+
+// Stream-K reduction assignment: whether CTA b sums part of tile t's pairs,
+// and which ([p0, p1) of `pairs`). Each contributor reduces in one tile
+// only — its only tile, or, when its share crosses a tile boundary, the one
+// it computed more of (the later one on a tie) — with a pair range in
+// proportion to its whole share; a tile that no contributor prefers is
+// reduced whole by its largest contributor. (When crossing CTAs also
+// reduced a slice of their second tile they waited for two tiles' partials
+// and ended the launch 3-4 us after the others on cfg1.) Computed the same
+// way by every thread from the share table: no per-launch table in Params.
+__device__ __forceinline__ bool sk_reduce_range(const Params& p, int b, int t, int pairs, int& p0,
+                                                int& p1, int& first, int& last) {
+  // 32-bit positions (the host keeps tiles * kblocks < 2^31); O(1): only the
+  // tile's first and last contributors can cross into a neighbour tile
+  const int kb = p.kblocks, t0k = t * kb, t1k = t0k + kb;
+  first = sk_owner(p, t0k);
+  last = sk_owner(p, t1k - 1);
+  if (first == last) return false;  // one contributor: it stored the whole tile itself
+  const int fa = p.sk_start[first], fe = p.sk_start[first + 1];
+  const int la = p.sk_start[last], le = p.sk_start[last + 1];
+  // first prefers t unless it computed more of t-1; last prefers t unless it
+  // computed at least as much of t+1 (ties go to the later tile)
+  const bool f_pref = fa == t0k || t0k - fa <= fe - t0k;
+  const bool l_pref = le <= t1k || t1k - la > le - t1k;
+  const int F = f_pref ? fe - fa : 0;
+  const int L = l_pref ? le - la : 0;
+  const int M = la - p.sk_start[first + 1];  // the contributors strictly inside t
+  const int W = F + M + L;
+  if (W == 0) {  // no contributor prefers t: the larger of the two sums it all
+    const int best = (fe - t0k) >= (t1k - la) ? first : last;
+    if (b != best) return false;
+    p0 = 0;
+    p1 = pairs;
+    return true;
   }
-  return lo;
+  int before, mine;
+  if (b == first) {
+    before = 0;
+    mine = F;
+  } else if (b == last) {
+    before = F + M;
+    mine = L;
+  } else if (b > first && b < last) {
+    before = F + p.sk_start[b] - p.sk_start[first + 1];
+    mine = p.sk_start[b + 1] - p.sk_start[b];
+  } else {
+    return false;
+  }
+  if (mine == 0) return false;
+  p0 = static_cast<int>(static_cast<int64_t>(pairs) * before / W);
+  p1 = static_cast<int>(static_cast<int64_t>(pairs) * (before + mine) / W);
+  return true;
 }
 
 // Wait for the gate (see Params), then order the async-proxy (TMA) operand
@@ -1008,13 +1059,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // in contributor (= k) order: bit-reproducible, spread over all of them.
     constexpr int PAIRS = BM * BN / 2;
     const bool use_beta = p.beta != 0.0;
+    const int my0 = p.sk_start[blockIdx.x], my1 = p.sk_start[blockIdx.x + 1];
+    int nred = 0;  // reductions done (trace marks of the first)
 #pragma unroll 1
-    for (int j = 0; j < 2; ++j) {
-      const int64_t t = p.red_tile[j][blockIdx.x];
-      if (t < 0) break;
-      const int tk0 = static_cast<int>(t * p.kblocks);
-      const int first = sk_owner(p, tk0);
-      const int S = sk_owner(p, tk0 + p.kblocks - 1) - first + 1;
+    for (int j = 0; j < 2 && my1 > my0; ++j) {
+      // this CTA's tiles: its share's first, then (if it crosses) its last
+      const int t = j == 0 ? my0 / p.kblocks : (my1 - 1) / p.kblocks;
+      if (j == 1 && t == my0 / p.kblocks) break;
+      int p0, p1, first, last;
+      if (!sk_reduce_range(p, blockIdx.x, t, PAIRS, p0, p1, first, last)) continue;
+      const int S = last - first + 1;
       const Unit un = decode_unit(p, t);
       consumer_sync();  // the previous tile's tables and slots are consumed
       {
@@ -1056,10 +1110,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         } while (seen < target);
       }
       consumer_sync();
-      if (j == 0) trace_mark(p, 4, tl);
+      if (nred == 0) trace_mark(p, 4, tl);
       const double2* ws = reinterpret_cast<const double2*>(p.ws);
-      const int p0 = p.red_p0[j][blockIdx.x];
-      const int p1 = p.red_p1[j][blockIdx.x];
       // Each thread owns up to RED pairs of the slice and issues 4 partial
       // loads per pair before summing (few L2 round trips, not S).
       constexpr int RED = 4;  // 2: -2 %, 8: -0.6 % on cfg1 (measured)
@@ -1113,7 +1165,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
-      if (j == 0) trace_mark(p, 5, tl);
+      if (nred == 0) trace_mark(p, 5, tl);
+      ++nred;
     }
   }
   trace_mark(p, 6, tl);
@@ -1684,66 +1737,6 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       if (p.sk_start[c + 1] > p.sk_start[c] &&
           (p.sk_start[c + 1] - 1) / kblocks - p.sk_start[c] / kblocks > 1)
         return set_error(TCB_EUNSUPPORTED, "gemm: stream-K share spans more than two tiles");
-    // reduction assignment (see Params::red_tile)
-    {
-      constexpr int64_t PAIRS = BM * BN / 2;
-      for (int j = 0; j < 2; ++j)
-        for (int c = 0; c < SK_MAX; ++c) {
-          p.red_tile[j][c] = -1;
-          p.red_p0[j][c] = p.red_p1[j][c] = 0;
-        }
-      auto w_of = [&](int c, int64_t t) {  // k-blocks of CTA c's share in tile t
-        const int64_t lo = std::max<int64_t>(p.sk_start[c], t * kblocks);
-        const int64_t hi = std::min<int64_t>(p.sk_start[c + 1], (t + 1) * kblocks);
-        return std::max<int64_t>(0, hi - lo);
-      };
-      auto tiles_of = [&](int c, int64_t& t0, int64_t& t1) {  // t1 = -1: one tile
-        t0 = t1 = -1;
-        if (p.sk_start[c + 1] <= p.sk_start[c]) return;
-        t0 = p.sk_start[c] / kblocks;
-        const int64_t tl = (p.sk_start[c + 1] - 1) / kblocks;
-        if (tl != t0) t1 = tl;
-      };
-      // preferred tile of each CTA: its only tile, or the one it computed
-      // more of (the later one on a tie)
-      std::vector<int64_t> pref(G, -1);
-      for (int c = 0; c < G; ++c) {
-        int64_t t0, t1;
-        tiles_of(c, t0, t1);
-        pref[c] = t1 < 0 ? t0 : (w_of(c, t0) > w_of(c, t1) ? t0 : t1);
-      }
-      int cf = 0;  // first contributor of tile t (two-pointer sweep)
-      for (int64_t t = dp; t < tiles; ++t) {
-        while (cf + 1 < G && p.sk_start[cf + 1] <= t * kblocks) ++cf;
-        int cl = cf;
-        while (cl + 1 < G && p.sk_start[cl + 1] <= (t + 1) * kblocks - 1) ++cl;
-        // reducers: contributors preferring t; else the largest contributor
-        std::vector<std::pair<int, int64_t>> red;  // (CTA, weight)
-        for (int c = cf; c <= cl; ++c) {
-          if (w_of(c, t) == 0 || pref[c] != t) continue;
-          red.emplace_back(c, p.sk_start[c + 1] - p.sk_start[c]);
-        }
-        if (red.empty()) {
-          int best = cf;
-          for (int c = cf; c <= cl; ++c)
-            if (w_of(c, t) > w_of(best, t)) best = c;
-          red.emplace_back(best, w_of(best, t));
-        }
-        int64_t W_t = 0;
-        for (const auto& r : red) W_t += r.second;
-        int64_t cum = 0;
-        for (const auto& r : red) {
-          const int c = r.first;
-          const int j = p.red_tile[0][c] < 0 ? 0 : 1;
-          if (j == 1 && p.red_tile[1][c] >= 0)
-            return set_error(TCB_EUNSUPPORTED, "gemm: stream-K reduction assignment");
-          p.red_tile[j][c] = static_cast<int>(t);
-          p.red_p0[j][c] = static_cast<int>(PAIRS * cum / W_t);
-          cum += r.second;
-          p.red_p1[j][c] = static_cast<int>(PAIRS * cum / W_t);
-        }
-      }
-    }
     // most contributors of one shared tile (reported), by a two-pointer sweep
     int c = 0;
     for (int64_t t = dp; t < tiles; ++t) {

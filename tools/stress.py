@@ -6,6 +6,7 @@ numpy.einsum (BLAS, fp64) at relative Frobenius <= 1e-12 (or, for results
 dominated by cancellation, the reference's max_rel_error <= 1e-12).
 Usage: python tools/stress.py [cases] [seed]"""
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -19,6 +20,7 @@ from specgen import random_spec
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 rng = np.random.default_rng(seed)
+verbose = os.environ.get("STRESS_VERBOSE") is not None  # print each case before running it
 EXT = (1, 2, 3, 5, 7, 13, 16, 17, 32, 48, 64, 96, 128, 130)
 
 
@@ -39,6 +41,8 @@ while done < cases:
     lt, rt = rhs.split("*")
     left = [t.strip()[1:] for t in lt.split("[")[1].rstrip("] ").split(",")]
     right = [t.strip()[1:] for t in rt.split("[")[1].rstrip("] ").split(",")]
+    if verbose:
+        print(json.dumps({"case": done, "expr": e, "extents": x}), flush=True)
     got, st = T.execute(e, x, seed=1)
     A = operand(left, ext, 1)
     B = operand(right, ext, 2)
