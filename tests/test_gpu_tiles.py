@@ -112,3 +112,19 @@ def test_short_k_with_scattered_output_is_race_free(dev, x):
         else:
             assert np.array_equal(out.view(np.uint64), first.view(np.uint64))
     p.close()
+
+
+@pytest.mark.parametrize("e,x", [
+    # batched stream-K with tiny tiles: 128 one-tile batches of 9 k-blocks on
+    # 148 CTAs (every tile shared by two CTAs; found by tools/stress.py seed 11)
+    ("R[+b,-a,+c,+g] = A[+e,-a] * B[+g,+c,-e,+b]", "e=130,a=7,g=2,c=3,b=128"),
+    # shares that cross tile boundaries with either neighbour preferred
+    ("C[+i,+j] = A[+i,+k] * B[-k,+j]", "i=300,j=260,k=1000"),
+    ("C[+i,+j,+b] = A[+i,+k,+b] * B[-k,+j,+b]", "i=100,j=60,k=700,b=40"),
+    # shares aligned to half tiles: two non-crossing contributors per tile
+    ("C[+i,+j,+b] = A[+i,+k,+b] * B[-k,+j,+b]", "i=128,j=128,k=128,b=37"),
+])
+def test_stream_k_reduction_assignment(dev, e, x):
+    L, R = O.operands(e, x, 3)
+    got, _ = T.execute(e, x, seed=3)
+    assert close(got, O.naive(e, x, L, R)), (e, x, T.lower(e, x))
