@@ -571,6 +571,10 @@ class PreparedContraction {
   std::int64_t launches_ = 0;
   struct Pipes;
   std::unique_ptr<Pipes> pipes_;  // streamed path: copy streams + events
+  // idle Pipes are pooled per device (process-wide) across prepared
+  // contractions: creating and destroying them costs ~0.1 ms each
+  static std::unique_ptr<Pipes> acquire_pipes(int device);
+  static void release_pipes(int device, std::unique_ptr<Pipes> p);
 };
 
 

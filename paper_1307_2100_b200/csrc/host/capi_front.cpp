@@ -1,4 +1,7 @@
 // Plan-level C-ABI (include/tcf.h) over the tc:: front. Host C++ only.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <random>
@@ -184,6 +187,8 @@ int tcf_execute_host(const char* expr, int positional, const char* extents, cons
                      int kernel, const char* s_left, const char* s_right, int64_t* stats,
                      double* seconds, char* err, int64_t errcap) {
   try {
+    static const bool trace = std::getenv("TC_EXEC_TRACE") != nullptr;  // diagnostics
+    const auto t0 = std::chrono::steady_clock::now();
     const tc::ContractionSpec spec = tc::parse(expr ? expr : "", positional != 0);
     const Shapes s = shapes_of(spec, parse_extents(extents));
     const tc::ValidatedContraction v = tc::validate_shapes(spec, s.le, s.lv, s.re, s.rv);
@@ -195,8 +200,16 @@ int tcf_execute_host(const char* expr, int positional, const char* extents, cons
     if (policy == 1) pol = tc::PlanPolicy::force_kernel(static_cast<tc::KernelKind>(kernel));
     if (policy == 2) pol = tc::PlanPolicy::force_slicing(vec_parse(s_left), vec_parse(s_right));
     const tc::ExecutionPlan p = tc::plan(v, pol);
+    if (trace)
+      std::fprintf(stderr, "front parse+plan %8.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
     static const auto backend = tc::make_b200_backend();
     const tc::ExecutionStats st = tc::execute_into(p, v, left, right, out, *backend, workers);
+    if (trace)
+      std::fprintf(stderr, "front returned   %8.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
     if (stats) {
       stats[0] = st.kernel_calls;
       stats[1] = st.packed_bytes;

@@ -19,6 +19,16 @@
 
 namespace tc {
 namespace {
+// TC_EXEC_TRACE=1 (diagnostics): host timestamps of the phases of a call
+// (ms since the call began) on stderr
+const bool kExecTrace = std::getenv("TC_EXEC_TRACE") != nullptr;
+thread_local std::chrono::steady_clock::time_point g_exec_t0 = std::chrono::steady_clock::now();
+void exec_mark(const char* what) {
+  if (kExecTrace)
+    std::fprintf(stderr, "execute %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                           g_exec_t0).count());
+}
 
 // Map a C-ABI status to the reference's exception types.
 void check(int status, const char* what) {
@@ -406,6 +416,44 @@ struct PreparedContraction::Pipes {
   }
 };
 
+namespace {
+constexpr int kPipesPoolDevices = 64;
+constexpr std::size_t kPipesPoolPerDevice = 8;
+std::mutex g_pipes_mu;
+// leaked on purpose: pooled streams live as long as the process (no
+// destruction order against the CUDA runtime at exit)
+std::vector<void*>* const g_pipes_free = new std::vector<void*>[kPipesPoolDevices];
+}  // namespace
+
+std::unique_ptr<PreparedContraction::Pipes> PreparedContraction::acquire_pipes(int device) {
+  if (device >= 0 && device < kPipesPoolDevices) {
+    std::lock_guard<std::mutex> lock(g_pipes_mu);
+    auto& v = g_pipes_free[device];
+    if (!v.empty()) {
+      std::unique_ptr<Pipes> p(static_cast<Pipes*>(v.back()));
+      v.pop_back();
+      return p;
+    }
+  }
+  return std::make_unique<Pipes>();
+}
+
+void PreparedContraction::release_pipes(int device, std::unique_ptr<Pipes> p) {
+  if (!p) return;
+  // idle before reuse: nothing pending, both copy streams drained
+  p->drain();
+  if (tcb_stream_sync(p->up) != TCB_OK || tcb_stream_sync(p->down) != TCB_OK) return;  // dropped
+  p->next = 0;
+  if (device >= 0 && device < kPipesPoolDevices) {
+    std::lock_guard<std::mutex> lock(g_pipes_mu);
+    auto& v = g_pipes_free[device];
+    if (v.size() < kPipesPoolPerDevice) {
+      v.push_back(p.release());
+      return;
+    }
+  }
+}
+
 PreparedContraction::PreparedContraction(const ValidatedContraction& v, int device)
     : v_(v), device_(device) {
   check(tcb_init(device_), "tcb_init");
@@ -444,7 +492,10 @@ PreparedContraction::PreparedContraction(const ValidatedContraction& v, int devi
 PreparedContraction::~PreparedContraction() {
   tcb_init(device_);
   tcb_sync();
-  pipes_.reset();
+  try {
+    release_pipes(device_, std::move(pipes_));
+  } catch (...) {  // drain() reports a failed sync by throwing: drop the pipes
+  }
   tcb_free(dl_);
   tcb_free(dr_);
   tcb_free(do_);
@@ -750,8 +801,10 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     return 1;
   }
 
-  if (!pipes_) pipes_ = std::make_unique<Pipes>();
+  exec_mark("o-slabs: lowered");
+  if (!pipes_) pipes_ = acquire_pipes(device_);
   Pipes& h = *pipes_;
+  exec_mark("o-slabs: pipes");
   h.next = 0;
   void* compute = tcb_current_stream();
   void* up = h.up;
@@ -816,7 +869,9 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
           "download");
     e0 += e;
   }
+  exec_mark("o-slabs: enqueued");
   h.finish(compute, wait, set_);
+  exec_mark("o-slabs: finished");
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
@@ -948,7 +1003,7 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
     }
     recipes.emplace(e, std::move(r));
   }
-  if (!pipes_) pipes_ = std::make_unique<Pipes>();
+  if (!pipes_) pipes_ = acquire_pipes(device_);
   Pipes& h = *pipes_;
   h.next = 0;
   void* compute = tcb_current_stream();
@@ -980,7 +1035,9 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
           "download");
     e0 += e;
   }
+  exec_mark("f-slabs: enqueued");
   h.finish(compute, wait, set_);
+  exec_mark("f-slabs: finished");
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
@@ -1072,6 +1129,7 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     if (!r.permutes.empty()) return nullptr;  // not expected (the full recipe permutes nothing)
     return &recipes.emplace(key, std::move(r)).first->second;
   };
+  exec_mark("k-slabs: sized");
   bool lowered = true;
   for (std::int64_t e : sizes) lowered = lowered && recipe(e, 0) != nullptr;
   for (int q = 0; q < parts && parts >= 2; ++q)
@@ -1097,8 +1155,10 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     o_sc = no_ / o_ext;
     if ((o_sa | o_sb | o_sc) & 1) parts = 1;  // block offsets would break 16-byte alignment
   }
-  if (!pipes_) pipes_ = std::make_unique<Pipes>();
+  exec_mark("k-slabs: lowered");
+  if (!pipes_) pipes_ = acquire_pipes(device_);
   Pipes& h = *pipes_;
+  exec_mark("k-slabs: pipes");
   h.next = 0;
   void* compute = tcb_current_stream();
   h.follow(compute, set_);
@@ -1153,7 +1213,9 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     check(tcb_stream_wait_event(h.down, done), "event");
     check(tcb_memcpy_async(out, do_, no_ * 8, h.down), "download");
   }
+  exec_mark("k-slabs: enqueued");
   h.finish(compute, wait, set_);
+  exec_mark("k-slabs: finished");
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
@@ -1179,14 +1241,8 @@ void check_plan(const ExecutionPlan& plan, const ValidatedContraction& v) {
 void run_on_device(const B200Backend& dev, const ValidatedContraction& v, const double* left,
                    const double* right, double* out, bool streamed, ExecutionStats& st,
                    const std::chrono::steady_clock::time_point& t0) {
-  // TC_EXEC_TRACE=1: phase times of this call on stderr (diagnostics)
-  static const bool trace = std::getenv("TC_EXEC_TRACE") != nullptr;
-  auto mark = [&](const char* what) {
-    if (trace)
-      std::fprintf(stderr, "execute %-10s %8.3f ms\n", what,
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
-                                                             t0).count());
-  };
+  g_exec_t0 = t0;
+  auto mark = [](const char* what) { exec_mark(what); };
   try {
     dev.tick("execute");
     PreparedContraction pc(v, dev.options().device);
@@ -1233,6 +1289,7 @@ ExecutionStats execute_into(const ExecutionPlan& plan, const ValidatedContractio
     const bool streamed =
         !off && host_pinned(out) && (host_pinned(left) || host_pinned(right));
     run_on_device(*dev, v, left, right, out, streamed, st, t0);
+    exec_mark("released");
   } else {
     std::int64_t n = 1;
     for (std::int64_t e : v.output_extents()) n *= e;
