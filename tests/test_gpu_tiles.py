@@ -120,9 +120,9 @@ def test_short_k_with_scattered_output_is_race_free(dev, x):
     ("R[+b,-a,+c,+g] = A[+e,-a] * B[+g,+c,-e,+b]", "e=130,a=7,g=2,c=3,b=128"),
     # shares that cross tile boundaries with either neighbour preferred
     ("C[+i,+j] = A[+i,+k] * B[-k,+j]", "i=300,j=260,k=1000"),
-    ("C[+i,+j,+b] = A[+i,+k,+b] * B[-k,+j,+b]", "i=100,j=60,k=700,b=40"),
+    ("C[+i,+j,+c] = A[+i,+k,+c] * B[-k,+j]", "i=100,j=60,k=700,c=40"),
     # shares aligned to half tiles: two non-crossing contributors per tile
-    ("C[+i,+j,+b] = A[+i,+k,+b] * B[-k,+j,+b]", "i=128,j=128,k=128,b=37"),
+    ("C[+i,+j,+c] = A[+i,+k,+c] * B[-k,+j]", "i=128,j=128,k=128,c=37"),
 ])
 def test_stream_k_reduction_assignment(dev, e, x):
     L, R = O.operands(e, x, 3)
