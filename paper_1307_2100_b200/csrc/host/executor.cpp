@@ -23,6 +23,29 @@ namespace {
 // (ms since the call began) on stderr
 const bool kExecTrace = std::getenv("TC_EXEC_TRACE") != nullptr;
 thread_local std::chrono::steady_clock::time_point g_exec_t0 = std::chrono::steady_clock::now();
+// TC_STREAM_TIMELINE=1 (diagnostics): device timestamps of the streamed
+// paths' copies and contractions (timed events), printed when the call waits
+struct Timeline {
+  const bool on = std::getenv("TC_STREAM_TIMELINE") != nullptr;
+  std::vector<std::pair<std::string, void*>> marks;
+  void mark(const std::string& what, void* stream) {
+    if (!on) return;
+    void* e = nullptr;
+    if (tcb_event_create_timed(&e) != TCB_OK) return;
+    tcb_event_record(e, stream);
+    marks.emplace_back(what, e);
+  }
+  void print() {
+    if (!on || marks.empty()) return;
+    for (auto& m : marks) {
+      float ms = 0.f;
+      tcb_event_elapsed(marks.front().second, m.second, &ms);
+      std::fprintf(stderr, "timeline %-28s %9.3f ms\n", m.first.c_str(), ms);
+    }
+    for (auto& m : marks) tcb_event_destroy(m.second);
+    marks.clear();
+  }
+};
 void exec_mark(const char* what) {
   if (kExecTrace)
     std::fprintf(stderr, "execute %-22s %8.3f ms\n", what,
@@ -1163,6 +1186,8 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   void* compute = tcb_current_stream();
   h.follow(compute, set_);
   const std::int64_t before = tcb_launch_count();
+  Timeline tl;
+  tl.mark("start", h.up);
   std::int64_t e0 = 0;
   for (int s = 0; s < slabs; ++s) {
     const std::int64_t e = sizes[static_cast<std::size_t>(s)];
@@ -1172,6 +1197,7 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     check(tcb_memcpy2d_async(dr_ + e0 * sb, sb * E * 8, right + e0 * sb, sb * E * 8, sb * e * 8,
                              hb, h.up),
           "upload");
+    tl.mark("slab " + std::to_string(s) + " (" + std::to_string(e) + ") up", h.up);
     // the slab's contraction waits for its uploads: on the device through the
     // gate where available, else through an event on the compute stream
     bool gated = h.gate_ok && tcb_stream_write_value(h.up, h.gate, h.gate_epoch + 1) == TCB_OK;
@@ -1192,6 +1218,7 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
       tcb_gemm_desc d = desc_of(*recipe(e, 0));
       d.beta = beta;
       gemm(d, dl_ + e0 * sa, dr_ + e0 * sb, do_);
+      tl.mark("slab " + std::to_string(s) + " gemm", compute);
     } else {
       for (int q = 0; q < parts; ++q) {
         const std::int64_t b0 = o_ext * q / parts, b1 = o_ext * (q + 1) / parts;
@@ -1201,8 +1228,10 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
         void* block_done = h.event();
         check(tcb_event_record(block_done, compute), "event");
         check(tcb_stream_wait_event(h.down, block_done), "event");
+        tl.mark("part " + std::to_string(q) + " gemm", compute);
         check(tcb_memcpy_async(out + b0 * o_sc, do_ + b0 * o_sc, (b1 - b0) * o_sc * 8, h.down),
               "download");
+        tl.mark("part " + std::to_string(q) + " down", h.down);
       }
     }
     e0 += e;
@@ -1216,6 +1245,7 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   exec_mark("k-slabs: enqueued");
   h.finish(compute, wait, set_);
   exec_mark("k-slabs: finished");
+  if (wait) tl.print();
   launches_ = tcb_launch_count() - before;
   return slabs;
 }
