@@ -1694,12 +1694,19 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       // TCB_SK_WASTE: idle-fraction threshold of the hybrid (diagnostics). The
       // hybrid's data-parallel phase stores C without the staged epilogue,
       // which costs short-k tiles a few per cent (cfg2 12 %, cfg3 2 %): 5 %
-      // by default, 0.4 % for tiles of >= 2048 k-blocks, whose epilogue is
-      // negligible (cfg5: 4096 tiles = 27.7 waves, 1.2 % idle in the last one:
-      // 987.9 -> 973.6 ms). Measured against it: the 256-k-block beta = 1 slab
-      // GEMMs of cfg5's streamed host path lose 2 % with the hybrid.
+      // by default, 0.4 % for long tiles, whose epilogue is negligible (cfg5:
+      // 4096 tiles = 27.7 waves, 1.2 % idle in the last one: 987.9 -> 973.6
+      // ms). A hybrid variant with the staged epilogue for its whole tiles (3
+      // stages) was measured slower than this one (6 stages) on every long-k
+      // shape (cfg5 988 vs 974 ms) and dropped.
       static const double waste_env = getenv("TCB_SK_WASTE") ? atof(getenv("TCB_SK_WASTE")) : -1;
-      const double waste = waste_env >= 0 ? waste_env : (kblocks >= 2048 ? 0.004 : 0.05);
+      // Measured (tools/slab_gemm_ab.py, cfg5-shaped 8192^2 GEMMs): the
+      // hybrid beats the staged data-parallel launch from 512 k-blocks per
+      // tile with beta = 0 (1.0-1.6 %: no last-wave tail, 6-stage ring) and
+      // from 768 with beta != 0 (its consumers read C themselves); cfg4 (256
+      // k-blocks, 110.7 waves) +0.3 %; cfg3 (64 k-blocks) -2 %.
+      const int64_t long_kb = d.beta == 0.0 ? 256 : 768;
+      const double waste = waste_env >= 0 ? waste_env : (kblocks >= long_kb ? 0.004 : 0.05);
       if (rem != 0 &&
           static_cast<double>(waves + 1) * sms > (1.0 + waste) * static_cast<double>(tiles) &&
           std::min<int64_t>(sms, rem * kblocks / 4) > rem) {
