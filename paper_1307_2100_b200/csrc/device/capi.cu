@@ -5,7 +5,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <mutex>
+#include <unordered_map>
+#include <map>
 #include <string>
 
 #include "tcb_internal.cuh"
@@ -167,6 +170,41 @@ static cudaMemPool_t device_pool() {
   return pools[dev & 63];
 }
 
+// Exact-size cache of idle device blocks in front of the stream-ordered pool.
+// The drop-in tc::execute allocates its operands and result per call; the
+// pool did not reliably hand the freed block back (cudaMallocAsync of cfg3's
+// 134 MB result took 0.2-7 ms — up to 109 ms — in about half the calls). A
+// freed block is idle (tcb_free synchronises the device first, like
+// cudaFree), so it can serve the next allocation of the same size on any
+// stream at once. Bounded (blocks and bytes per device); flushed back to the
+// pool when an allocation fails and by tcb_finalize. The pool itself keeps
+// freed memory reserved anyway (release threshold: never).
+namespace {
+constexpr int kCacheMaxBlocks = 32;
+constexpr int64_t kCacheMaxBytes = 64LL << 30;
+struct BlockCache {
+  std::mutex mu;
+  std::unordered_map<void*, int64_t> live[64];        // tcb_alloc'ed blocks -> size
+  std::multimap<int64_t, void*> idle[64];             // cached idle blocks by size
+  int64_t idle_bytes[64] = {};
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache;  // process lifetime (no exit-order issues)
+  return *c;
+}
+// back to the pool: every cached block of the device (stream-ordered free)
+void flush_cache(int dev, cudaStream_t stream) {
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  for (auto& kv : c.idle[dev]) {
+    c.live[dev].erase(kv.second);
+    cudaFreeAsync(kv.second, stream);
+  }
+  c.idle[dev].clear();
+  c.idle_bytes[dev] = 0;
+}
+}  // namespace
+
 int tcb_finalize(void) {
   // releases the calling thread's state on every device it used
   ThreadCtx& c = ctx();
@@ -177,6 +215,8 @@ int tcb_finalize(void) {
     if (st.stream) cudaStreamSynchronize(st.stream);
     if (cudaMemPool_t pool = device_pool()) {  // hand cached blocks back to the driver
       cudaDeviceSynchronize();
+      flush_cache(d, st.stream);
+      cudaStreamSynchronize(st.stream);
       cudaMemPoolTrimTo(pool, 0);
     }
     if (st.ws) cudaFree(st.ws);
@@ -238,17 +278,33 @@ int tcb_alloc(void** dptr, int64_t bytes) {
   if (!dptr || bytes < 0) return set_error(TCB_EINVAL, "tcb_alloc: bad argument");
   *dptr = nullptr;
   if (bytes == 0) return TCB_OK;
-  cudaMemPool_t pool = device_pool();
   ThreadState& st = state();
+  const int dev = st.device & 63;
+  BlockCache& cache = block_cache();
+  {
+    std::lock_guard<std::mutex> lock(cache.mu);
+    auto it = cache.idle[dev].find(bytes);
+    if (it != cache.idle[dev].end()) {
+      *dptr = it->second;
+      cache.idle[dev].erase(it);
+      cache.idle_bytes[dev] -= bytes;
+      return TCB_OK;
+    }
+  }
+  cudaMemPool_t pool = device_pool();
   cudaError_t e = cudaMallocAsync(dptr, static_cast<size_t>(bytes), st.stream);
-  if (e == cudaErrorMemoryAllocation && pool) {
+  if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     cudaDeviceSynchronize();
-    cudaMemPoolTrimTo(pool, 0);
+    flush_cache(dev, st.stream);
+    cudaStreamSynchronize(st.stream);
+    if (pool) cudaMemPoolTrimTo(pool, 0);
     e = cudaMallocAsync(dptr, static_cast<size_t>(bytes), st.stream);
   }
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
   TCB_CUDA(cudaStreamSynchronize(st.stream));  // usable on every stream, like cudaMalloc
+  std::lock_guard<std::mutex> lock(cache.mu);
+  cache.live[dev][*dptr] = bytes;
   return TCB_OK;
 }
 
@@ -256,7 +312,24 @@ int tcb_free(void* dptr) {
   if (!dptr) return TCB_OK;
   TCB_TRY_INIT();
   TCB_CUDA(cudaDeviceSynchronize());  // cudaFree's implicit synchronisation
-  TCB_CUDA(cudaFreeAsync(dptr, state().stream));
+  ThreadState& st = state();
+  const int dev = st.device & 63;
+  BlockCache& cache = block_cache();
+  {
+    std::lock_guard<std::mutex> lock(cache.mu);
+    auto it = cache.live[dev].find(dptr);
+    if (it != cache.live[dev].end()) {
+      const int64_t bytes = it->second;
+      if (static_cast<int>(cache.idle[dev].size()) < kCacheMaxBlocks &&
+          cache.idle_bytes[dev] + bytes <= kCacheMaxBytes) {
+        cache.idle[dev].emplace(bytes, dptr);  // idle now (device synchronised)
+        cache.idle_bytes[dev] += bytes;
+        return TCB_OK;
+      }
+      cache.live[dev].erase(it);
+    }
+  }
+  TCB_CUDA(cudaFreeAsync(dptr, st.stream));
   return TCB_OK;
 }
 

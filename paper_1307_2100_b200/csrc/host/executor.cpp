@@ -480,7 +480,9 @@ void PreparedContraction::release_pipes(int device, std::unique_ptr<Pipes> p) {
 PreparedContraction::PreparedContraction(const ValidatedContraction& v, int device)
     : v_(v), device_(device) {
   check(tcb_init(device_), "tcb_init");
+  exec_mark("prepare: init");
   recipe_ = lower_checked(v, &groups_ok_);
+  exec_mark("prepare: lowered");
   nl_ = 1;
   for (int m = 0; m < v.left_rank(); ++m) nl_ *= v.label_at_left_mode(m).extent;
   nr_ = 1;
@@ -494,10 +496,13 @@ PreparedContraction::PreparedContraction(const ValidatedContraction& v, int devi
   try {
     check(tcb_alloc(&p, nl_ * 8), "device allocation");
     dl_ = static_cast<double*>(p);
+    exec_mark("prepare: alloc left");
     check(tcb_alloc(&p, nr_ * 8), "device allocation");
     dr_ = static_cast<double*>(p);
+    exec_mark("prepare: alloc right");
     check(tcb_alloc(&p, no_ * 8), "device allocation");
     do_ = static_cast<double*>(p);
+    exec_mark("prepare: alloc out");
     for (const PermuteStep& ps : recipe_.permutes) {
       check(tcb_alloc(&p, ps.elements * 8), "device allocation");
       (ps.right ? pr_ : pl_) = static_cast<double*>(p);
