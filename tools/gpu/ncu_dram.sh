@@ -7,7 +7,8 @@ python - "$cfg" "$tag" <<'PY'
 import csv, sys
 cfg, tag = sys.argv[1], sys.argv[2]
 rows = [r for r in csv.reader(open(f"gpurun_out/ncu_{cfg}_{tag}.csv")) if len(r) > 5]
-hdr = rows[0]; vals = {}
+hi = next(i for i, r in enumerate(rows) if "Metric Name" in r)
+hdr = rows[hi]; rows = rows[hi:]; vals = {}
 for r in rows[1:]:
     d = dict(zip(hdr, r)); vals[d["Metric Name"]] = (d["Metric Unit"], d["Metric Value"])
 def g(k):
