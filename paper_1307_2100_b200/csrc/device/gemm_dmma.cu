@@ -158,6 +158,9 @@ struct Params {
   // 2 = evict_last): the raster's resident panel group evict_last, the
   // streamed operand evict_first, so the stream does not push the group out
   int a_hint, b_hint, c_hint;
+  // prefetch each whole tile's C into L2 ahead of its epilogue (beta != 0
+  // with a register-path epilogue; plain column-major C, no batch)
+  int c_pf;
 };
 
 // Params + three tensor maps are the kernel's parameters: stay within the
@@ -547,6 +550,7 @@ struct LoadIter {
   int ca[5], cb[5];      // TMA: outer + batch coordinates of the segment's tile
   int mirror;            // >= 0: k-blocks issued as mirror - kb (descending)
   bool valid;
+  bool whole;            // the segment is a whole tile
 
   template <bool USE_TMA>
   __device__ __forceinline__ void start(const Params& p) {
@@ -558,6 +562,7 @@ struct LoadIter {
     int64_t tile;
     valid = it.next(p, tile, kb, kb1);
     if (!valid) return;
+    whole = kb == 0 && kb1 == p.kblocks;
     mirror = (p.kflip && kb == 0 && kb1 == p.kblocks &&
               ((static_cast<unsigned>(tile) / gridDim.x) & 1u))
                  ? kb1 - 1
@@ -856,6 +861,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       else
         issue_stage<A_KMAJOR, B_KMAJOR, USE_TMA>(p, tmA, tmB, li, s_base + s * STAGE_BYTES,
                                                  full0 + 8 * s, tid);
+      if (p.c_pf && li.kb + 1 == li.kb1 && li.kb1 == p.kblocks && li.whole) {
+        // beta != 0, C read by a register-path epilogue: prefetch the tile of
+        // C into L2 with the tile's last operand loads (one bulk prefetch per
+        // column; the consumers are still NST k-blocks behind)
+        const double* c0 = p.C + li.m0 + static_cast<int64_t>(li.n0) * p.c_col_str[0];
+        const int64_t rows = min(static_cast<int64_t>(BM), p.M - li.m0);
+        const uint32_t bytes = static_cast<uint32_t>((rows * 8 + 15) & ~15LL);
+        const int cols = static_cast<int>(min(static_cast<int64_t>(BN), p.N - li.n0));
+#pragma unroll 1
+        for (int j = 0; j < cols; ++j)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c0 + j * p.c_col_str[0]),
+                       "r"(bytes)
+                       : "memory");
+      }
       ++g;
       li.template advance<USE_TMA>(p);
     }
@@ -1803,6 +1822,13 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     const char* cwhy = nullptr;
     p.c_tma = make_cmap(&tc, &p.pc, C, d, BM, &cwhy) ? 1 : 0;
   }
+  // TCB_NO_CPF=1 disables it (diagnostics)
+  static const bool no_cpf = getenv("TCB_NO_CPF") != nullptr;
+  p.c_pf = (!no_cpf && tma && d.beta != 0.0 && !p.c_tma && d.nbatch == 0 && d.c_nrow == 1 &&
+            d.c_ncol == 1 && d.c_row_str[0] == 1 && d.c_col_str[0] % 2 == 0 &&
+            reinterpret_cast<uintptr_t>(C) % 16 == 0 && kblocks >= 16)
+               ? 1
+               : 0;
 
   const int grid = streamk ? G : static_cast<int>(std::min<int64_t>(tiles, sms));
 
