@@ -1927,7 +1927,7 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
     // TCB_PACE=<shift>,<slack> (diagnostics): epoch 2^shift k-blocks, slack in epochs
     static const char* pe = getenv("TCB_PACE");
     static const int kShift = pe ? std::max(1, atoi(pe)) : 4;
-    static const int kSlack = (pe && strchr(pe, ',')) ? std::max(1, atoi(strchr(pe, ',') + 1)) : 2;
+    static const int kSlack = (pe && strchr(pe, ',')) ? std::max(1, atoi(strchr(pe, ',') + 1)) : 1;
     if (!no_pace && tma && kblocks >= 128 && maxkb >= (8LL << kShift) &&
         make_pace_ready(st)) {
       static const bool no_flip = getenv("TCB_NO_KFLIP") != nullptr;
