@@ -311,6 +311,66 @@ __device__ __forceinline__ constexpr int kstep_k(int j, int q) {
   return (q & 1) | ((q >> 1) << 2) | ((j & 1) << 1) | ((j >> 1) << 3);
 }
 
+// One k-block of a consumer warp: 4 k-steps of 12 fragment loads + 32 DMMA.
+// EPI != 0 (the last k-block of a segment): the last k-step's DMMAs are
+// interleaved with the accumulators' stores, LAG DMMAs behind the one that
+// finishes each accumulator, so the tensor pipe keeps issuing while the tile
+// leaves the registers — EPI 1: into the staging tile of the staged epilogue
+// (a separate store pass idles the pipe for ~0.4 us per tile: 128 KB at the
+// shared-memory store rate); EPI 2: a stream-K partial into its workspace
+// slot (`part`: this thread's first pair, pairs CTHREADS apart).
+template <bool A_KMAJOR, bool B_KMAJOR, int EPI>
+__device__ __forceinline__ void consume_kblock(double (&acc)[8][4][2], uint32_t sA, uint32_t sB,
+                                               const uint32_t (&offA)[4],
+                                               const uint32_t (&offB)[4], int wm, int wn,
+                                               uint32_t stg, double2* part, int r, int q) {
+  constexpr int LAG = 6;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double a[8], b[4];
+#pragma unroll
+    for (int im = 0; im < 8; ++im) {
+      const uint32_t addr = A_KMAJOR ? sA + (wm * 64 + im * 8) * 128 + offA[j]
+                                     : sA + (wm * 4 + (im >> 1)) * 2048 + (j >> 1) * 1024 +
+                                           offA[(j & 1) | ((im & 1) << 1)];
+      a[im] = lds64(addr);
+    }
+#pragma unroll
+    for (int in = 0; in < 4; ++in) {
+      const uint32_t addr = B_KMAJOR ? sB + (wn * 32 + in * 8) * 128 + offB[j]
+                                     : sB + (wn * 2 + (in >> 1)) * 2048 + (j >> 1) * 1024 +
+                                           offB[(j & 1) | ((in & 1) << 1)];
+      b[in] = lds64(addr);
+    }
+    if (EPI != 0 && j == 3) {
+#pragma unroll
+      for (int v = 0; v < 32 + LAG; ++v) {
+        if (v < 32) dmma(acc[v >> 2][v & 3], a[v >> 2], b[v & 3]);
+        if (v >= LAG) {
+          const int im = (v - LAG) >> 2, in = (v - LAG) & 3;
+          if (EPI == 2) {
+            asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(part + (im * 4 + in) * CTHREADS),
+                         "d"(acc[im][in][0]), "d"(acc[im][in][1])
+                         : "memory");
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const uint32_t ad =
+                  stg + stage_off(wm * 64 + im * 8 + r, wn * 32 + in * 8 + 2 * q + jj);
+              asm volatile("st.shared.f64 [%0], %1;" ::"r"(ad), "d"(acc[im][in][jj]) : "memory");
+            }
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int im = 0; im < 8; ++im)
+#pragma unroll
+        for (int in = 0; in < 4; ++in) dmma(acc[im][in], a[im], b[in]);
+    }
+  }
+}
+
 // ------------------------------------------------------------- unit decode
 // Index arithmetic below is 32-bit unsigned: the host guarantees units,
 // batch count, M and N (and every group extent) are < 2^31, so no 64-bit
@@ -928,8 +988,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    // Staged epilogue woven into the tile's last k-block (see consume_kblock):
+    // alpha == 1 only (the scaling would put DMULs between the DMMAs);
+    // TCB_DIAG bit 64 keeps the separate store pass for A/B timing.
+    const bool weave = STAGED && !p.alpha_ne1 && !(p.diag & 64);
+    // likewise a stream-K segment's partial tile into its workspace slot
+    const bool weave_sk = SPLITK && (kb0 != 0 || kb1 != p.kblocks) && !(p.diag & 64);
+    const int kb_main = (weave || weave_sk) ? kb1 - 1 : kb1;
 #pragma unroll 1
-    for (int kb = kb0; kb < kb1; ++kb) {
+    for (int kb = kb0; kb < kb_main; ++kb) {
       const uint32_t stage = gcons % NST;
       mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
       if (p.trace != nullptr) {  // diagnostics only: one uniform branch per k-block
@@ -941,30 +1008,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (tcount == 2 && kb == kb0 + 8) trace_mark(p, 31, tl);
       }
       const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        double a[8], b[4];
-#pragma unroll
-        for (int im = 0; im < 8; ++im) {
-          const uint32_t addr =
-              A_KMAJOR ? sA + (wm * 64 + im * 8) * 128 + offA[j]
-                       : sA + (wm * 4 + (im >> 1)) * 2048 + (j >> 1) * 1024 +
-                             offA[(j & 1) | ((im & 1) << 1)];
-          a[im] = lds64(addr);
-        }
-#pragma unroll
-        for (int in = 0; in < 4; ++in) {
-          const uint32_t addr =
-              B_KMAJOR ? sB + (wn * 32 + in * 8) * 128 + offB[j]
-                       : sB + (wn * 2 + (in >> 1)) * 2048 + (j >> 1) * 1024 +
-                             offB[(j & 1) | ((in & 1) << 1)];
-          b[in] = lds64(addr);
-        }
-#pragma unroll
-        for (int im = 0; im < 8; ++im)
-#pragma unroll
-          for (int in = 0; in < 4; ++in) dmma(acc[im][in], a[im], b[in]);
-      }
+      consume_kblock<A_KMAJOR, B_KMAJOR, 0>(acc, sA, sB, offA, offB, wm, wn, 0u, nullptr, r, q);
       // Release the stage only once every lane's fragment loads from it have
       // completed: ptxas issues the arrive as soon as the loads are issued
       // (their DMMAs may follow it), and the producer's next TMA write to the
@@ -975,6 +1019,59 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(empty0 + 8 * stage);
       ++gcons;
+    }
+    if constexpr (STAGED) {
+      if (weave) {
+        const uint32_t stage = gcons % NST;
+        mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
+        if (p.trace != nullptr) {
+          if (kb_main == kb0 && tcount > 0 && tcount <= 8)
+            trace_mark(p, 10 + 3 * (static_cast<int>(tcount) - 1), tl);
+          if (gcons == 0) trace_mark(p, 1, tl);
+          if (tcount == 0) trace_mark(p, 2, tl);
+          if (tcount < 8) trace_mark(p, 8 + 3 * static_cast<int>(tcount), tl);
+        }
+        // the storer has drained the previous tile (a tile earlier: no wait in practice)
+        mbar_wait(stg_empty, (tcount & 1) ^ 1);
+        const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
+        consume_kblock<A_KMAJOR, B_KMAJOR, 1>(acc, sA, sB, offA, offB, wm, wn,
+                                              smem_u32(staging), nullptr, r, q);
+        asm volatile("fence.acq_rel.cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+        ++gcons;
+        fence_proxy_async_smem();  // the TMA store reads the tile through the async proxy
+        mbar_arrive(stg_full);
+        if (tcount < 8) trace_mark(p, 9 + 3 * static_cast<int>(tcount), tl);
+        continue;
+      }
+    }
+    if constexpr (SPLITK) {
+      if (weave_sk) {
+        // Stream-K partial (see the separate pass below for the slot layout),
+        // stored while the segment's last DMMAs issue; no output tables needed.
+        const uint32_t stage = gcons % NST;
+        mbar_wait(full0 + 8 * stage, (gcons / NST) & 1);
+        if (p.trace != nullptr) {
+          if (gcons == 0) trace_mark(p, 1, tl);
+          if (tcount == 0) trace_mark(p, 2, tl);
+        }
+        pdl_wait();  // the previous grid may still read the workspace / counters
+        double2* part = reinterpret_cast<double2*>(p.ws) +
+                        (2 * static_cast<int64_t>(blockIdx.x) + npart) * (BM * BN / 2) + ctid;
+        const uint32_t sA = s_base + stage * STAGE_BYTES, sB = sA + STAGE_A;
+        consume_kblock<A_KMAJOR, B_KMAJOR, 2>(acc, sA, sB, offA, offB, wm, wn, 0u, part, r, q);
+        asm volatile("fence.acq_rel.cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+        ++gcons;
+        consumer_sync();
+        if (npart == 0) trace_mark(p, 3, tl);
+        if (ctid == 0)
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + u) : "memory");
+        ++npart;
+        continue;
+      }
     }
 
     // ------------------------------ epilogue ------------------------------
