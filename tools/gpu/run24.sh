@@ -1,7 +1,7 @@
-# re-entry check on a fresh box: GPU suite, smoke, both bench arms with wall-clock
-set -x
-mkdir -p gpurun_out/r24
-( time python -m pytest tests -m gpu -x -q ) > gpurun_out/r24/gputests.log 2>&1; tail -5 gpurun_out/r24/gputests.log
-( time python -c "import __graft_entry__ as g; g.smoke()" ) > gpurun_out/r24/smoke.log 2>&1; tail -12 gpurun_out/r24/smoke.log
-( time python bench.py --impl reference ) > gpurun_out/r24/bench_ref.log 2>&1; tail -4 gpurun_out/r24/bench_ref.log
-( time python bench.py ) > gpurun_out/r24/bench.log 2>&1; tail -4 gpurun_out/r24/bench.log
+b() { python bench.py --config $1 --steps $2 --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print('$1', '$3', d['value'], d['ms_per_step'], d['roofline']['frac'], d['parity_ok'], d['gpu_launches'])"; }
+n() { timeout 300 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:dgemm -s 1 -c 1 --csv python tools/prof.py $1 2 2>/dev/null | grep -E "dram__|gpu__time" | awk -F'","' '{print "'$1' '$2'", $(NF-2), $NF}'; }
+for mb in 16 32 48; do
+TCB_L2PERSIST_MB=$mb b cfg4 30 p$mb
+TCB_L2PERSIST_MB=$mb n cfg4 p$mb
+done
+TCB_NO_L2PERSIST=1 b cfg4 30 nopersist
