@@ -475,11 +475,17 @@ def fill_operands(expr: str, full: str, label: str | None, lo: int, hi: int, L, 
         raise errs[0]
 
 
+# (steps, warmup) when the command line names none
+DEFAULT_STEPS = {"cfg1": (300, 20), "cfg2": (200, 10), "cfg3": (50, 5), "cfg4": (10, 3),
+                 "cfg5": (10, 3)}
+
+
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: per config, see DEFAULT_STEPS)")
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -491,6 +497,14 @@ def main() -> int:
                     help="keeping L2-sized working sets cold: rotate over copies or flush")
     args = ap.parse_args()
     cfg = args.config
+    # without flags: enough steps that the timed region is tens of ms at least
+    # (ten 70-us steps of cfg1 end before the SM clock has settled: 0.77 of
+    # peak against 0.81 over 300 steps on the same box)
+    ours = args.impl == "ours"  # the CPU arm's steps are seconds each: 10 / 3
+    if args.steps is None:
+        args.steps = DEFAULT_STEPS[cfg][0] if ours else 10
+    if args.warmup is None:
+        args.warmup = DEFAULT_STEPS[cfg][1] if ours else 3
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     if os.environ.get("TCB_BENCH_EXTENTS"):  # plumbing tests only, never a BASELINE number

@@ -757,6 +757,69 @@ __device__ __forceinline__ void store_tile(const double (&acc)[8][4][2], double*
   }
 }
 
+// Stream-K fix-up: sum pairs [p0, p1) of a tile over its S contributors'
+// workspace slots in contributor (= k) order and write them to C.
+// Each thread owns up to RED pairs per pass and issues the partial loads of CB
+// contributors before summing.
+constexpr int SK_RED_CB = 10;
+template <int CB>
+__device__ __forceinline__ void sk_reduce_pairs(const Params& p, const double2* ws,
+                                                const int* s_slot, const int64_t* s_row,
+                                                const int64_t* s_col, double* Cb, int S, int p0,
+                                                int p1, int ctid, bool use_beta) {
+  constexpr int PAIRS = BM * BN / 2;
+  constexpr int RED = 4;  // 2: -2 %, 8: -0.6 % on cfg1 (measured)
+#pragma unroll 1
+  for (int pb = p0 + ctid; pb < p1; pb += CTHREADS * RED) {
+    double2 sum[RED];
+#pragma unroll
+    for (int i = 0; i < RED; ++i) sum[i] = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int sp0 = 0; sp0 < S; sp0 += CB) {
+      double2 v[CB][RED];
+#pragma unroll
+      for (int jj = 0; jj < CB; ++jj) {
+        const int64_t base = sp0 + jj < S ? static_cast<int64_t>(s_slot[sp0 + jj]) * PAIRS : 0;
+#pragma unroll
+        for (int i = 0; i < RED; ++i) {
+          const int pi = pb + i * CTHREADS;
+          v[jj][i] = (sp0 + jj < S && pi < p1) ? __ldcg(ws + base + pi) : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < CB; ++jj)
+#pragma unroll
+        for (int i = 0; i < RED; ++i)
+          if (sp0 + jj < S) {  // contributor order 0..S-1
+            sum[i].x += v[jj][i].x;
+            sum[i].y += v[jj][i].y;
+          }
+    }
+#pragma unroll
+    for (int i = 0; i < RED; ++i) {
+      const int pi = pb + i * CTHREADS;
+      if (pi >= p1) continue;
+      // pair index -> (m, n): v = pi / 256 (im = v/4, in = v%4), thread t = pi % 256
+      const int v = pi >> 8, tt = pi & 255;
+      const int tw = tt >> 5, tl2 = tt & 31;
+      const int m = (tw & 1) * 64 + (v >> 2) * 8 + (tl2 >> 2);
+      const int n = (tw >> 1) * 32 + (v & 3) * 8 + 2 * (tl2 & 3);
+      const int64_t roff = s_row[m];
+      if (roff < 0) continue;
+      const double sv[2] = {sum[i].x, sum[i].y};
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int64_t coff = s_col[n + jj];
+        if (coff < 0) continue;
+        double* dst = Cb + roff + coff;
+        double vv = p.alpha * sv[jj];
+        if (use_beta) vv += p.beta * *dst;
+        *dst = vv;
+      }
+    }
+  }
+}
+
 // 384 threads: warpgroup 0 = producer (TMA: one elected thread; cp.async: all
 // 128), warpgroups 1-2 = 8 DMMA consumer warps. setmaxnreg moves registers
 // from the producer (40/thread) to the consumers (232/thread) so the 64-double
@@ -1228,59 +1291,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       consumer_sync();
       if (nred == 0) trace_mark(p, 4, tl);
       const double2* ws = reinterpret_cast<const double2*>(p.ws);
-      // Each thread owns up to RED pairs of the slice and issues 4 partial
-      // loads per pair before summing (few L2 round trips, not S).
-      constexpr int RED = 4;  // 2: -2 %, 8: -0.6 % on cfg1 (measured)
-#pragma unroll 1
-      for (int pb = p0 + ctid; pb < p1; pb += CTHREADS * RED) {
-        double2 sum[RED];
-#pragma unroll
-        for (int i = 0; i < RED; ++i) sum[i] = make_double2(0.0, 0.0);
-#pragma unroll 1
-        for (int sp0 = 0; sp0 < S; sp0 += 4) {
-          double2 v[4][RED];
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int64_t base = sp0 + jj < S ? static_cast<int64_t>(s_slot[sp0 + jj]) * PAIRS : 0;
-#pragma unroll
-            for (int i = 0; i < RED; ++i) {
-              const int pi = pb + i * CTHREADS;
-              v[jj][i] = (sp0 + jj < S && pi < p1) ? __ldcg(ws + base + pi)
-                                                   : make_double2(0.0, 0.0);
-            }
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-            for (int i = 0; i < RED; ++i)
-              if (sp0 + jj < S) {  // contributor order 0..S-1
-                sum[i].x += v[jj][i].x;
-                sum[i].y += v[jj][i].y;
-              }
-        }
-#pragma unroll
-        for (int i = 0; i < RED; ++i) {
-          const int pi = pb + i * CTHREADS;
-          if (pi >= p1) continue;
-          // pair index -> (m, n): v = pi / 256 (im = v/4, in = v%4), thread t = pi % 256
-          const int v = pi >> 8, tt = pi & 255;
-          const int tw = tt >> 5, tl2 = tt & 31;
-          const int m = (tw & 1) * 64 + (v >> 2) * 8 + (tl2 >> 2);
-          const int n = (tw >> 1) * 32 + (v & 3) * 8 + 2 * (tl2 & 3);
-          const int64_t roff = s_row[m];
-          if (roff < 0) continue;
-          const double sv[2] = {sum[i].x, sum[i].y};
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const int64_t coff = s_col[n + jj];
-            if (coff < 0) continue;
-            double* dst = Cb + roff + coff;
-            double vv = p.alpha * sv[jj];
-            if (use_beta) vv += p.beta * *dst;
-            *dst = vv;
-          }
-        }
-      }
+      // Each thread owns up to RED pairs of the slice and has the partials of
+      // up to CB contributors in flight before summing (one L2 round trip for
+      // a tile shared by <= CB CTAs instead of one per 4 contributors).
+      if (p.diag & 128)  // TCB_DIAG bit 128: the 4-contributor batches (A/B timing)
+        sk_reduce_pairs<4>(p, ws, s_slot, s_row, s_col, Cb, S, p0, p1, ctid, use_beta);
+      else
+        sk_reduce_pairs<SK_RED_CB>(p, ws, s_slot, s_row, s_col, Cb, S, p0, p1, ctid, use_beta);
       if (nred == 0) trace_mark(p, 5, tl);
       ++nred;
     }
