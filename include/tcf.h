@@ -112,6 +112,19 @@ int tcf_tensor_text(const int64_t* ext, int rank, const char* var, uint64_t seed
 int tcf_read_tensor_text(const char* text, double* out, int64_t cap, int64_t* n, char* err,
                          int64_t errcap);
 
+/* ---- metric tensors (tc::invert_metric / lower_index / raise_index;
+ * reference include/tc/metric.hpp:17-32) — a caller of the contraction path -
+ * g: n x n column-major, symmetric (down, down). Status 1 with the
+ * reference's messages ("metric is not symmetric", "metric is singular", ...). */
+int tcf_invert_metric(int64_t n, const double* g, double* g_inv, char* err, int64_t errcap);
+/* t (extents ext[0..rank), variances var as "+-" chars) with mode `mode`
+ * contracted against g (raise == 0: lower_index, the mode must be '+') or
+ * against g's inverse (raise != 0: raise_index, the mode must be '-'), through
+ * validate -> plan -> execute on the b200 backend; out has t's shape. */
+int tcf_metric_apply(const int64_t* ext, int rank, const char* var, const double* t, int mode,
+                     int64_t n, const double* g, int raise, double* out, int64_t out_cap,
+                     char* err, int64_t errcap);
+
 /* ---- benchmark sweep (tc::run_bench + tc::write_bench_csv; reference
  * include/tc/bench.hpp:13-51) ----------------------------------------------
  * sizes "150,200"; kernels "GEMM,COPY+GEMM,..."; custom_extents "a=3,b=4".

@@ -21,7 +21,8 @@ from .native import GemmDesc, GemmInfo, TcbError, check
 KERNELS = ["GEMM", "COPY+GEMM", "GEMV", "COPY+GEMV", "GER", "DOT", "ELEMENTWISE"]
 
 __all__ = ["report", "lower", "execute", "execute_host", "seeded", "Prepared", "DeviceBuffer", "GemmDesc", "GemmInfo",
-           "TcbError", "check", "native", "KERNELS", "parse_expr"]
+           "TcbError", "check", "native", "KERNELS", "parse_expr", "invert_metric",
+           "metric_apply"]
 
 
 def _err(code: int, buf) -> None:
@@ -151,6 +152,39 @@ def read_tensor_text(text: str) -> np.ndarray:
         C.POINTER(C.c_double)), cap, C.byref(n), err, len(err))
     _err(rc, err)
     return out[:n.value].copy()
+
+
+def invert_metric(g: np.ndarray) -> np.ndarray:
+    """tc::invert_metric (reference include/tc/metric.hpp:17-19): the inverse
+    of a symmetric n x n metric; ValueError with the reference's messages."""
+    g = np.asfortranarray(g, dtype=np.float64)
+    if g.ndim != 2 or g.shape[0] != g.shape[1]:
+        raise ValueError("metric must be a square rank-2 tensor")
+    out = np.empty_like(g, order="F")
+    err = C.create_string_buffer(4096)
+    pd = C.POINTER(C.c_double)
+    rc = native.front().tcf_invert_metric(g.shape[0], g.ctypes.data_as(pd),
+                                          out.ctypes.data_as(pd), err, len(err))
+    _err(rc, err)
+    return out
+
+
+def metric_apply(t: np.ndarray, variance: str, mode: int, g: np.ndarray,
+                 raise_: bool = False) -> np.ndarray:
+    """tc::lower_index (raise_ False) / tc::raise_index (True) of mode `mode`
+    of t (Fortran order, variances as "+-" chars) with the metric g, on the
+    b200 backend (reference include/tc/metric.hpp:24-32)."""
+    t = np.asfortranarray(t, dtype=np.float64)
+    g = np.asfortranarray(g, dtype=np.float64)
+    out = np.empty_like(t, order="F")
+    ext = (C.c_int64 * max(1, t.ndim))(*t.shape)
+    err = C.create_string_buffer(4096)
+    pd = C.POINTER(C.c_double)
+    rc = native.front().tcf_metric_apply(ext, t.ndim, variance.encode(), t.ctypes.data_as(pd),
+                                         mode, g.shape[0], g.ctypes.data_as(pd), int(raise_),
+                                         out.ctypes.data_as(pd), out.size, err, len(err))
+    _err(rc, err)
+    return out
 
 
 def bench_csv(experiment: str = "square3d", sizes=(100,), kernels=("GEMM",),

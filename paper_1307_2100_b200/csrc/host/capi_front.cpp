@@ -8,6 +8,7 @@
 #include <sstream>
 #include <string>
 
+#include "tc/metric.hpp"
 #include "tc/contract.hpp"
 #include "tcb.h"
 #include "tcf.h"
@@ -454,6 +455,42 @@ int tcf_read_tensor_text(const char* text, double* out, int64_t cap, int64_t* n,
     if (n) *n = t.size();
     if (t.size() > cap) return 4;
     std::memcpy(out, t.data(), static_cast<std::size_t>(t.size()) * 8);
+    return 0;
+  }
+  TCF_GUARD(err, errcap)
+}
+
+int tcf_invert_metric(int64_t n, const double* g, double* g_inv, char* err, int64_t errcap) {
+  try {
+    if (n < 0 || !g || !g_inv) throw std::invalid_argument("bad metric buffers");
+    tc::Tensor G = tc::Tensor::zeros({n, n}, {tc::Variance::Down, tc::Variance::Down}, "g");
+    std::memcpy(G.data(), g, static_cast<std::size_t>(n * n) * 8);
+    const tc::MetricTensor m = tc::invert_metric(G);
+    std::memcpy(g_inv, m.g_inv.data(), static_cast<std::size_t>(n * n) * 8);
+    return 0;
+  }
+  TCF_GUARD(err, errcap)
+}
+
+int tcf_metric_apply(const int64_t* ext, int rank, const char* var, const double* t, int mode,
+                     int64_t n, const double* g, int raise, double* out, int64_t out_cap,
+                     char* err, int64_t errcap) {
+  try {
+    if (rank < 0 || (rank > 0 && (!ext || !var)) || !t || !g || !out)
+      throw std::invalid_argument("bad tensor shape");
+    std::vector<std::int64_t> e(ext, ext + rank);
+    std::vector<tc::Variance> v;
+    for (int i = 0; i < rank; ++i) v.push_back(var[i] == '-' ? tc::Variance::Down : tc::Variance::Up);
+    tc::Tensor T = tc::Tensor::zeros(std::move(e), std::move(v), "t");
+    std::memcpy(T.data(), t, static_cast<std::size_t>(T.size()) * 8);
+    tc::Tensor G = tc::Tensor::zeros({n, n}, {tc::Variance::Down, tc::Variance::Down}, "g");
+    std::memcpy(G.data(), g, static_cast<std::size_t>(n * n) * 8);
+    const tc::MetricTensor m = tc::invert_metric(G);
+    const auto backend = tc::make_backend("b200");
+    const tc::Tensor r = raise ? tc::raise_index(T, mode, m, *backend)
+                               : tc::lower_index(T, mode, m, *backend);
+    if (r.size() > out_cap) return 4;
+    std::memcpy(out, r.data(), static_cast<std::size_t>(r.size()) * 8);
     return 0;
   }
   TCF_GUARD(err, errcap)

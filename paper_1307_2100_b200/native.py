@@ -139,6 +139,8 @@ TCF_API = {
     "tcf_last_error": (cp, []),
     "tcf_tensor_text": (i32, [P_i64, i32, cp, C.c_uint64, cp, cp, i64]),
     "tcf_read_tensor_text": (i32, [cp, P_f64, i64, P_i64, cp, i64]),
+    "tcf_invert_metric": (i32, [i64, P_f64, P_f64, cp, i64]),
+    "tcf_metric_apply": (i32, [P_i64, i32, cp, P_f64, i32, i64, P_f64, i32, P_f64, i64, cp, i64]),
     "tcf_bench_csv": (i32, [cp, cp, cp, cp, i32, C.c_uint64, i32, i32, cp, cp, cp, i64,
                             C.POINTER(C.c_int)]),
 }

@@ -8,6 +8,7 @@
 #include "helpers.hpp"
 #include "tc/executor.hpp"
 #include "tc/kernels.hpp"
+#include "tc/metric.hpp"
 #include "tc/oracle.hpp"
 
 using namespace tc;
@@ -173,6 +174,105 @@ TEST_CASE("backend gemm/gemv/ger/dot known answers on host pointers") {  // test
   CHECK_THROWS_AS(kBackend->gemm(false, false, 2, 2, 2, 1.0, Z.data(), 1, Z.data(), 2, 0.0,
                                  Z.data(), 2),
                   std::invalid_argument);
+}
+
+// ------------------------------------------------------ metric (tc/metric.hpp)
+// lower_index / raise_index on the device (reference tests/test_metric.cpp)
+namespace {
+MetricTensor dense3() {
+  return invert_metric(Tensor::from_values({3, 3}, {Variance::Down, Variance::Down},
+                                           {4, 1, 0.5, 1, 3, 0.25, 0.5, 0.25, 2}));
+}
+}  // namespace
+
+TEST_CASE("metric lowering on the device: diagonal products, round trip, commuting modes") {
+  const double r = 2.0, th = M_PI / 2;
+  const auto sph = spherical_metric(r, th);
+  const Tensor S = Tensor::seeded_random({3, 3}, {Variance::Up, Variance::Up}, 17, "S");
+  const Tensor low = lower_index(lower_index(S, 0, sph, *kBackend), 1, sph, *kBackend);
+  const double d[3] = {1.0, r * r, r * r * std::sin(th) * std::sin(th)};
+  for (std::int64_t i = 0; i < 3; ++i)
+    for (std::int64_t j = 0; j < 3; ++j)
+      CHECK(std::fabs(low.at({i, j}) - d[i] * d[j] * S.at({i, j})) <= 1e-12 * 16);
+  CHECK(low.variance(0) == Variance::Down);
+  CHECK(low.variance(1) == Variance::Down);
+
+  const auto m = dense3();
+  const Tensor t =
+      Tensor::seeded_random({3, 4, 3}, {Variance::Up, Variance::Down, Variance::Up}, 5);
+  for (const int mode : {0, 2}) {
+    const Tensor back = raise_index(lower_index(t, mode, m, *kBackend), mode, m, *kBackend);
+    CHECK(max_rel_error(back, t) <= 1e-10);
+  }
+  // a metric dimension that spans several tiles: 200 x 200 SPD, rank-3 tensor
+  const std::int64_t n = 200;
+  Tensor g = Tensor::zeros({n, n}, {Variance::Down, Variance::Down});
+  const Tensor noise = Tensor::seeded_random({n, n}, {Variance::Down, Variance::Down}, 77);
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t j = 0; j < n; ++j)
+      g.data()[i + j * n] = (i == j ? 8.0 : 0.0) +
+                            0.01 * (noise.data()[i + j * n] + noise.data()[j + i * n]);
+  const auto big = invert_metric(g);
+  const Tensor w = Tensor::seeded_random({37, n, 5}, {Variance::Down, Variance::Up, Variance::Up}, 6);
+  const Tensor wl = lower_index(w, 1, big, *kBackend);
+  CHECK(wl.variance(1) == Variance::Down);
+  // against the direct sum over the contracted mode
+  double worst = 0, scale = 1;
+  for (std::int64_t c = 0; c < 5; ++c)
+    for (std::int64_t x = 0; x < n; x += 17)
+      for (std::int64_t a = 0; a < 37; a += 5) {
+        double acc = 0;
+        for (std::int64_t y = 0; y < n; ++y) acc += w.at({a, y, c}) * big.g.at({y, x});
+        worst = std::max(worst, std::fabs(acc - wl.at({a, x, c})));
+        scale = std::max(scale, std::fabs(acc));
+      }
+  CHECK(worst / scale <= 1e-12);
+  CHECK(max_rel_error(raise_index(wl, 1, big, *kBackend), w) <= 1e-10);
+}
+
+TEST_CASE("metric placements: both routes agree and all six match the oracle") {  // :153-218
+  const auto m = dense3();
+  const Tensor T = Tensor::seeded_random({2, 2, 3}, std::vector<Variance>(3, Variance::Up), 21, "T");
+  const Tensor S = Tensor::seeded_random({3, 2}, std::vector<Variance>(2, Variance::Up), 22, "S");
+  const Tensor Tl = lower_index(T, 2, m, *kBackend);
+  const auto v1 = validate(parse("R[+a,+b,+r] = T[+a,+b,-s] * S[+s,+r]"), Tl, S);
+  const Tensor r1 = execute(plan(v1), v1, Tl, S, *kBackend).first;
+  const Tensor Sl = lower_index(S, 0, m, *kBackend);
+  const auto v2 = validate(parse("R[+a,+b,+r] = T[+a,+b,+s] * S[-s,+r]"), T, Sl);
+  const Tensor r2 = execute(plan(v2), v2, T, Sl, *kBackend).first;
+  CHECK(max_rel_error(r1, r2) <= 1e-12);
+
+  const Tensor T3 = Tensor::seeded_random({3, 3, 3}, std::vector<Variance>(3, Variance::Up), 33, "T");
+  const Tensor S3 = Tensor::seeded_random({3, 3}, std::vector<Variance>(2, Variance::Up), 34, "S");
+  const char* names[3] = {"a", "b", "c"};
+  for (int t_mode = 0; t_mode < 3; ++t_mode)
+    for (int s_mode = 0; s_mode < 2; ++s_mode) {
+      const Tensor low = lower_index(T3, t_mode, m, *kBackend);
+      ContractionSpec spec;
+      spec.left.name = "T";
+      spec.right.name = "S";
+      spec.output.name = "R";
+      for (int k = 0; k < 3; ++k) {
+        if (k == t_mode) {
+          spec.left.indices.push_back({"s", Variance::Down});
+        } else {
+          spec.left.indices.push_back({names[k], Variance::Up});
+          spec.output.indices.push_back({names[k], Variance::Up});
+        }
+      }
+      for (int k = 0; k < 2; ++k) {
+        if (k == s_mode) {
+          spec.right.indices.push_back({"s", Variance::Up});
+        } else {
+          spec.right.indices.push_back({"r", Variance::Up});
+          spec.output.indices.push_back({"r", Variance::Up});
+        }
+      }
+      const auto v = validate(spec, low, S3);
+      const Tensor got = execute(plan(v), v, low, S3, *kBackend).first;
+      CHECK(max_rel_error(got, contract_naive(v, low, S3)) <= 1e-12);
+      CHECK(max_rel_error(got, naive(v, low, S3)) <= 1e-12);
+    }
 }
 
 TH_MAIN

@@ -6,6 +6,8 @@
 
 #include "harness.hpp"
 #include "helpers.hpp"
+#include "tc/metric.hpp"
+#include "tc/tensor_io.hpp"
 
 using namespace tc;
 using tst::bind_expr;
@@ -381,6 +383,137 @@ TEST_CASE("execute_into with a caller's backend fills caller storage") {
   for (std::size_t i = 0; i < want.size(); ++i) worst = std::max(worst, std::fabs(out[i] - want[i]));
   CHECK(worst <= 1e-13);
   CHECK(st.kernel_calls == 2);  // one GEMM per c slice
+}
+
+// ------------------------------------------------------ metric (tc/metric.hpp)
+// Restated from the reference's tests/test_metric.cpp; the contractions run
+// slice by slice through the host test backend (no device in this suite).
+namespace {
+Tensor diagonal(std::initializer_list<double> d) {
+  const auto n = static_cast<std::int64_t>(d.size());
+  Tensor g = Tensor::zeros({n, n}, {Variance::Down, Variance::Down}, "g");
+  std::int64_t i = 0;
+  for (double x : d) g.data()[(i++) * (n + 1)] = x;
+  return g;
+}
+const std::vector<double> kDense3{4, 1, 0.5, 1, 3, 0.25, 0.5, 0.25, 2};
+bool near(double a, double b, double tol = 1e-12) { return std::fabs(a - b) <= tol * std::max(1.0, std::fabs(b)); }
+}  // namespace
+
+TEST_CASE("invert_metric: identity, diagonal, dense symmetric") {  // test_metric.cpp:28-60
+  const auto id = invert_metric(diagonal({1, 1, 1}));
+  CHECK(id.dimension == 3);
+  for (int i = 0; i < 3; ++i) CHECK(id.g_inv.at({i, i}) == 1.0);
+  const auto m = invert_metric(diagonal({1, 4, 4}));
+  CHECK(near(m.g_inv.at({0, 0}), 1.0));
+  CHECK(near(m.g_inv.at({1, 1}), 0.25));
+  CHECK(near(m.g_inv.at({2, 2}), 0.25));
+  CHECK(m.g_inv.at({0, 1}) == 0.0);
+  CHECK(m.g_inv.variance(0) == Variance::Up);
+  CHECK(m.g.variance(1) == Variance::Down);
+
+  const auto d = invert_metric(
+      Tensor::from_values({3, 3}, {Variance::Down, Variance::Down}, kDense3));
+  for (std::int64_t i = 0; i < 3; ++i)
+    for (std::int64_t j = 0; j < 3; ++j) {
+      double acc = 0;
+      for (std::int64_t k = 0; k < 3; ++k) acc += d.g.at({i, k}) * d.g_inv.at({k, j});
+      CHECK(near(acc, i == j ? 1.0 : 0.0, 1e-14));
+    }
+  // a larger ill-scaled but regular case: pivoting must pick the big entries
+  const std::int64_t n = 6;
+  Tensor g = Tensor::zeros({n, n}, {Variance::Down, Variance::Down});
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t j = 0; j < n; ++j)
+      g.data()[i + j * n] = (i == j ? 1e-3 * static_cast<double>(i + 1) : 0.0) +
+                            1.0 / static_cast<double>(1 + i + j);
+  const auto h = invert_metric(g);
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t j = 0; j < n; ++j) {
+      double acc = 0;
+      for (std::int64_t k = 0; k < n; ++k) acc += h.g.at({i, k}) * h.g_inv.at({k, j});
+      CHECK(near(acc, i == j ? 1.0 : 0.0, 1e-9));
+    }
+}
+
+TEST_CASE("invert_metric rejects bad input with the reference's messages") {  // :39-47
+  Tensor g = diagonal({1, 2, 3});
+  g.at({0, 1}) = 0.5;
+  CHECK_THROWS_WITH_AS(invert_metric(g), "metric is not symmetric", std::invalid_argument);
+  CHECK_THROWS_WITH_AS(invert_metric(diagonal({1, 0, 1})), "metric is singular",
+                       std::invalid_argument);
+  CHECK_THROWS_WITH_AS(invert_metric(Tensor::zeros({2, 3}, {Variance::Down, Variance::Down})),
+                       "metric must be a square rank-2 tensor", std::invalid_argument);
+  CHECK_THROWS_AS(invert_metric(diagonal({1.0, 1e-30, 1.0})), std::invalid_argument);
+  CHECK_THROWS_WITH_AS(invert_metric(diagonal({1.0, 1e-13, 1.0})),
+                       "metric is numerically singular", std::invalid_argument);
+}
+
+TEST_CASE("spherical metric values and singular points") {  // :62-76
+  const auto unit = spherical_metric(1.0, M_PI / 2);
+  for (int i = 0; i < 3; ++i) CHECK(near(unit.g.at({i, i}), 1.0));
+  const auto m = spherical_metric(2.0, M_PI / 2);
+  CHECK(near(m.g.at({1, 1}), 4.0));
+  CHECK(near(m.g.at({2, 2}), 4.0));
+  CHECK(near(m.g_inv.at({2, 2}), 0.25));
+  CHECK(near(spherical_metric(2.0, M_PI / 6).g.at({2, 2}), 1.0));
+  CHECK_THROWS_AS(spherical_metric(0.0, 1.0), std::invalid_argument);
+  CHECK_THROWS_AS(spherical_metric(1.0, 0.0), std::invalid_argument);
+}
+
+TEST_CASE("lowering and raising through a caller's backend") {  // :78-151
+  HostBlas be;
+  const auto id = invert_metric(diagonal({1, 1, 1}));
+  const Tensor t = Tensor::seeded_random({3, 3}, {Variance::Up, Variance::Up}, 3);
+  const Tensor low = lower_index(t, 1, id, be);
+  CHECK(low.variance(1) == Variance::Down);
+  CHECK(low.variance(0) == Variance::Up);
+  for (std::int64_t i = 0; i < t.size(); ++i) CHECK(near(low.data()[i], t.data()[i], 1e-14));
+  CHECK(be.calls > 0);
+
+  const auto sph = spherical_metric(2.0, M_PI / 2);
+  const Tensor v = Tensor::from_values({3}, {Variance::Up}, {1, 1, 1}, "v");
+  const Tensor lv = lower_index(v, 0, sph, be);
+  CHECK(near(lv.at({0}), 1.0));
+  CHECK(near(lv.at({1}), 4.0));
+  CHECK(near(lv.at({2}), 4.0));
+  const Tensor back = raise_index(lv, 0, invert_metric(diagonal({1, 4, 4})), be);
+  for (int i = 0; i < 3; ++i) CHECK(near(back.at({i}), 1.0));
+
+  const auto dense = invert_metric(
+      Tensor::from_values({3, 3}, {Variance::Down, Variance::Down}, kDense3));
+  const Tensor w =
+      Tensor::seeded_random({3, 4, 3}, {Variance::Up, Variance::Down, Variance::Up}, 5);
+  for (const int mode : {0, 2}) {
+    const Tensor rt = raise_index(lower_index(w, mode, dense, be), mode, dense, be);
+    CHECK(max_rel_error(rt, w) <= 1e-10);
+  }
+  // lowering distinct modes commutes
+  const auto m2 = invert_metric(
+      Tensor::from_values({2, 2}, {Variance::Down, Variance::Down}, {2, 0.5, 0.5, 3}));
+  const Tensor c = Tensor::seeded_random({2, 2, 2}, std::vector<Variance>(3, Variance::Up), 9);
+  CHECK(max_rel_error(lower_index(lower_index(c, 0, m2, be), 2, m2, be),
+                      lower_index(lower_index(c, 2, m2, be), 0, m2, be)) <= 1e-12);
+}
+
+TEST_CASE("metric variance, extent and mode guards") {  // :134-142, src/metric.cpp:64-70
+  HostBlas be;
+  const auto m = spherical_metric(2.0, 1.0);
+  CHECK_THROWS_WITH_AS(lower_index(Tensor::zeros({3}, {Variance::Down}), 0, m, be),
+                       "mode is already lowered", std::invalid_argument);
+  CHECK_THROWS_WITH_AS(raise_index(Tensor::zeros({3}, {Variance::Up}), 0, m, be),
+                       "mode is already raised", std::invalid_argument);
+  CHECK_THROWS_WITH_AS(lower_index(Tensor::zeros({4}, {Variance::Up}), 0, m, be),
+                       "mode extent does not match metric dimension", std::invalid_argument);
+  CHECK_THROWS_WITH_AS(lower_index(Tensor::zeros({3}, {Variance::Up}), 1, m, be),
+                       "mode out of range", std::invalid_argument);
+}
+
+TEST_CASE("metrics serialize through the tensor text format") {  // :220-226
+  const auto m = spherical_metric(2.0, M_PI / 3);
+  std::stringstream ss;
+  write_tensor(ss, m.g);
+  CHECK(max_rel_error(read_tensor(ss), m.g) == 0.0);
 }
 
 TH_MAIN
