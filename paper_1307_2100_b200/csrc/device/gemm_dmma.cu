@@ -127,6 +127,7 @@ struct Params {
   // staged epilogue: C written by one TMA tensor store per tile (c_tma) with
   // coordinate program pc (sources: 0 m origin, 1 n origin, 2 batch)
   int c_tma;
+  int c_red;                  // beta == 1: the TMA store is a reduce-add into C
   MapProg pc;
   // tile raster: groups of `raster_g` m-tiles per n sweep (raster_n = 0), or
   // of raster_g n-tiles per m sweep (raster_n = 1, keeps that set of B panels
@@ -231,6 +232,17 @@ __device__ __forceinline__ void tma_store5(const CUtensorMap* map, uint32_t src,
                                            int c2, int c3, int c4) {
   asm volatile(
       "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
+      " [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// C += tile: the TMA engine adds the staged tile to C in L2 (one f64 add per
+// element, so fma(1, C, v) exactly) — beta == 1 without a single C load by the SM
+__device__ __forceinline__ void tma_reduce_add5(const CUtensorMap* map, uint32_t src, int c0,
+                                                int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.tile.bulk_group"
       " [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(reinterpret_cast<uint64_t>(map)),
       "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src)
       : "memory");
@@ -734,26 +746,48 @@ __device__ __forceinline__ void issue_stage(const Params& p, const CUtensorMap& 
 }
 
 // Epilogue: thread's 8x4x2 accumulators -> C through the tile's offset tables.
+// BETA: the old C values of two accumulator rows (16 loads) are fetched
+// before any of their stores. Written element by element (load, DFMA, store)
+// the compiler must keep every load behind the previous store (the pointers
+// may alias for all it knows), which serialises 64 L2 round trips per tile:
+// ~22 us per 128 x 128 tile, 0.5 % of a cfg5 K-slab GEMM (SASS: LDG, DFMA,
+// STG chains; measured 122.4 vs 121.8 ms for a 64-l slab with beta = 1 / 0).
 template <bool BETA>
 __device__ __forceinline__ void store_tile(const double (&acc)[8][4][2], double* Cb,
                                            const int64_t* s_row, const int64_t (&coff)[4][2],
                                            const bool (&cok)[4][2], int wm, int r, double alpha,
                                            double beta) {
+  constexpr int G = 2;  // accumulator rows per batch of old-C loads
 #pragma unroll
-  for (int im = 0; im < 8; ++im) {
-    const int64_t roff = s_row[wm * 64 + im * 8 + r];
-    double* row = Cb + roff;
-    const bool rok = roff >= 0;
+  for (int im0 = 0; im0 < 8; im0 += G) {
+    double* row[G];
+    bool rok[G];
+    double old[G][4][2];
 #pragma unroll
-    for (int in = 0; in < 4; ++in)
+    for (int g = 0; g < G; ++g) {
+      const int64_t roff = s_row[wm * 64 + (im0 + g) * 8 + r];
+      row[g] = Cb + roff;
+      rok[g] = roff >= 0;
+    }
+    if (BETA) {
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const bool ok = rok && cok[in][jj];
-        double* dst = row + coff[in][jj];
-        double v = alpha * acc[im][in][jj];
-        if (BETA) v = fma(beta, ok ? *dst : 0.0, v);
-        if (ok) *dst = v;
-      }
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int in = 0; in < 4; ++in)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj)
+            old[g][in][jj] = (rok[g] && cok[in][jj]) ? *(row[g] + coff[in][jj]) : 0.0;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int in = 0; in < 4; ++in)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          double v = alpha * acc[im0 + g][in][jj];
+          if (BETA) v = fma(beta, old[g][in][jj], v);
+          if (rok[g] && cok[in][jj]) *(row[g] + coff[in][jj]) = v;
+        }
   }
 }
 
@@ -901,7 +935,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           mbar_wait(stg_full, t & 1);
           pdl_wait();
-          if (p.c_hint)
+          if (p.c_red)
+            tma_reduce_add5(&tmC, stg, c[0], c[1], c[2], c[3], c[4]);
+          else if (p.c_hint)
             tma_store5_hint(&tmC, stg, c[0], c[1], c[2], c[3], c[4], l2_policy(p.c_hint));
           else if (!(p.diag & 16))  // TCB_DIAG bit 16: no C store (timing experiment)
             tma_store5(&tmC, stg, c[0], c[1], c[2], c[3], c[4]);
@@ -935,23 +971,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // alpha was applied by the consumers; plain copies keep the FP64 pipe
         // (shared with DMMA) free unless beta needs a DFMA.
         const bool use_beta = p.beta_nz != 0;  // host-side flag: no FP64 compare here
-#pragma unroll 1
-        for (int n = swarp; n < BN; n += 3) {
-          const int64_t coff = s_col[n];
-          double v[BM / 32];
-          int64_t roff[BM / 32];
+        int64_t roff[BM / 32];
 #pragma unroll
-          for (int j = 0; j < BM / 32; ++j) {
-            const int m = slane + 32 * j;
-            roff[j] = s_row[m];
-            v[j] = lds64(smem_u32(staging) + stage_off(m, n));
+        for (int j = 0; j < BM / 32; ++j) roff[j] = s_row[slane + 32 * j];
+        if (use_beta && !(p.diag & 1)) {
+          // beta: the old values of column n + 3 are fetched before column n
+          // is combined and stored (two columns' L2 round trips in flight per
+          // warp; element by element the loads could not pass the previous
+          // stores, and a tile of 16 k-blocks waited ~60 us for its storers)
+          double old[BM / 32];
+          {
+            const int64_t c0 = s_col[swarp];
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              old[j] = (c0 >= 0 && roff[j] >= 0) ? Cb[roff[j] + c0] : 0.0;
           }
+#pragma unroll 1
+          for (int n = swarp; n < BN; n += 3) {
+            const int64_t coff = s_col[n];
+            const int64_t cnext = n + 3 < BN ? s_col[n + 3] : -1;
+            double nxt[BM / 32];
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              nxt[j] = (cnext >= 0 && roff[j] >= 0) ? Cb[roff[j] + cnext] : 0.0;
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j) {
+              const double v = lds64(smem_u32(staging) + stage_off(slane + 32 * j, n));
+              if (coff >= 0 && roff[j] >= 0) Cb[roff[j] + coff] = fma(p.beta, old[j], v);
+            }
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j) old[j] = nxt[j];
+          }
+        } else {
+#pragma unroll 1
+          for (int n = swarp; n < BN; n += 3) {
+            const int64_t coff = s_col[n];
+            double v[BM / 32];
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              v[j] = lds64(smem_u32(staging) + stage_off(slane + 32 * j, n));
             if (coff < 0 || (p.diag & 1)) continue;
 #pragma unroll
-          for (int j = 0; j < BM / 32; ++j) {
-            if (roff[j] < 0) continue;
-            double* dst = Cb + roff[j] + coff;
-            *dst = use_beta ? fma(p.beta, *dst, v[j]) : v[j];
+            for (int j = 0; j < BM / 32; ++j)
+              if (roff[j] >= 0) Cb[roff[j] + coff] = v[j];
           }
         }
         // the staging loads must have completed before the consumers may
@@ -1838,7 +1900,8 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
       // tile with beta = 0 (1.0-1.6 %: no last-wave tail, 6-stage ring) and
       // from 768 with beta != 0 (its consumers read C themselves); cfg4 (256
       // k-blocks, 110.7 waves) +0.3 %; cfg3 (64 k-blocks) -2 %.
-      const int64_t long_kb = d.beta == 0.0 ? 256 : 768;
+      static const int64_t long_kb_env = getenv("TCB_SK_LONGKB") ? atoll(getenv("TCB_SK_LONGKB")) : 0;
+      const int64_t long_kb = long_kb_env > 0 ? long_kb_env : (d.beta == 0.0 ? 256 : 768);
       const double waste = waste_env >= 0 ? waste_env : (kblocks >= long_kb ? 0.004 : 0.05);
       if (rem != 0 &&
           static_cast<double>(waves + 1) * sms > (1.0 + waste) * static_cast<double>(tiles) &&
@@ -1927,14 +1990,20 @@ int launch_gemm(const tcb_gemm_desc& d, const double* A, const double* B, double
                    make_map(&tb, &p.pb, B, b_k, g.bn, g.bk, d, d.bat_sb, &why);
   // index groups are read through the tensor maps only
   if (!tma && has_groups(d)) return set_error(TCB_EUNSUPPORTED, std::string("gemm: index groups: ") + why);
-  // staged epilogue: C by TMA store when beta == 0 and the map describes C
+  // staged epilogue: C by TMA store when beta == 0 and the map describes C;
+  // beta == 1 (accumulation, the reference loop nest's case) by a TMA
+  // reduce-add of the same tile (TCB_NO_CRED=1: the storers' load / DFMA /
+  // store path instead, diagnostics)
   CUtensorMap tc;
   std::memset(&tc, 0, sizeof tc);
   static const bool no_cstore = getenv("TCB_NO_CSTORE") != nullptr;  // diagnostics
+  static const bool no_cred = getenv("TCB_NO_CRED") != nullptr;
   p.c_tma = 0;
-  if (tma && !streamk && d.beta == 0.0 && !no_cstore) {
+  p.c_red = 0;
+  if (tma && !streamk && (d.beta == 0.0 || (d.beta == 1.0 && !no_cred)) && !no_cstore) {
     const char* cwhy = nullptr;
     p.c_tma = make_cmap(&tc, &p.pc, C, d, BM, &cwhy) ? 1 : 0;
+    p.c_red = (p.c_tma && d.beta == 1.0) ? 1 : 0;
   }
   // TCB_NO_CPF=1 disables it (diagnostics)
   static const bool no_cpf = getenv("TCB_NO_CPF") != nullptr;

@@ -61,6 +61,37 @@ def test_beta_accumulate_through_tma_store_shapes(dev):
         assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref)), (m, n, k, beta)
 
 
+@pytest.mark.parametrize("m,n,k,alpha", [(2048, 2048, 256, 1.0), (4096, 4096, 512, 0.75),
+                                         (1000, 1234, 96, 1.0), (4096, 4096, 2048, 1.0),
+                                         (8192, 4096, 16384, 1.0)])
+def test_beta_one_is_one_exact_addition(dev, m, n, k, alpha):
+    """beta == 1: the staged tile is added to C by a TMA reduce-add (one f64
+    add per element in L2), the long-k hybrid's consumers add the old values
+    they loaded in batches: either way C_new == C_old + (alpha A B) bit for
+    bit, where alpha A B is the same launch with beta == 0 (shapes whose
+    beta == 0 and beta == 1 launches take the same tile schedule: below 256
+    or from 768 k-blocks per tile). Ragged edges (1000 x 1234) are clipped by
+    the tensor map."""
+    import ctypes as C
+    from paper_1307_2100_b200 import DeviceBuffer as D
+    dA, dB = D(m * k * 8), D(k * n * 8)
+    rng = np.random.default_rng(m + k)
+    blk = rng.uniform(-1, 1, 1 << 22)
+    for buf, cnt in ((dA, m * k), (dB, k * n)):
+        for off in range(0, cnt, blk.size):
+            c = min(blk.size, cnt - off)
+            T.check(dev.tcb_h2d(buf.ptr + off * 8, blk.ctypes.data, c * 8))
+    C0 = rng.uniform(-1, 1, m * n)
+    dC = D.from_array(np.zeros(m * n))
+    T.check(dev.tcb_dgemm(0, 0, m, n, k, alpha, dA.ptr, m, dB.ptr, k, 0.0, dC.ptr, m))
+    prod = dC.to_array(m * n)
+    dC2 = D.from_array(C0)
+    T.check(dev.tcb_dgemm(0, 0, m, n, k, alpha, dA.ptr, m, dB.ptr, k, 1.0, dC2.ptr, m))
+    got = dC2.to_array(m * n)
+    assert np.array_equal(got, C0 + prod), (m, n, k, alpha)
+    assert np.abs(prod).max() > 0
+
+
 @pytest.mark.parametrize("m,n,k,beta", [(2048, 2048, 128, 0.0), (2048, 2048, 128, -1.5),
                                         (1536, 2560, 256, 0.5), (300, 200, 4096, 2.0)])
 def test_stream_k_hybrid_and_pure_shapes_with_beta(dev, m, n, k, beta):
