@@ -94,6 +94,46 @@ def test_gemm_vs_long_double_oracle(dev, seed):
     assert paths & {0, 1}
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_gemm_accumulate_beta_one_random_shapes(dev, seed):
+    # beta == 1 (the reference loop nest's accumulation, src/executor.cpp:162)
+    # over even / odd leading dimensions, padded ldc, transposes, one- and
+    # multi-wave grids: the TMA reduce-add epilogue, the register epilogue and
+    # the cp.async variant, against the long-double oracle; the padding rows of
+    # C (ldc > m) must stay untouched
+    rng = np.random.default_rng(300 + seed)
+    paths = set()
+    for it in range(24):
+        if it % 4 == 0:
+            m, n = (int(v) for v in rng.integers(900, 2600, 2))
+            k = int(rng.integers(16, 700))
+        elif it % 4 == 1:
+            m, n, k = (int(v) for v in rng.integers(100, 700, 3))
+        else:
+            m, n, k = (int(v) for v in rng.integers(1, 200, 3))
+        if it % 2 == 0:  # TMA-legal: even leading dimensions
+            m += m % 2
+            k += k % 2
+            n += n % 2
+        ta, tb = int(rng.integers(2)), int(rng.integers(2))
+        pad = 2 * int(rng.integers(0, 3))
+        lda, ldb, ldc = (k if ta else m) + pad, (n if tb else k) + pad, m + pad
+        a = rng.uniform(-1, 1, lda * (m if ta else k))
+        b = rng.uniform(-1, 1, ldb * (k if tb else n))
+        c = rng.uniform(-1, 1, ldc * n)
+        alpha = 1.0 if it % 3 else -0.75
+        want = c.copy()
+        O.tco().tco_gemm_check(ta, tb, m, n, k, alpha, a.ctypes.data, lda, b.ctypes.data, ldb,
+                               1.0, want.ctypes.data, ldc)
+        got = dgemm(dev, ta, tb, m, n, k, alpha, a, lda, b, ldb, 1.0, c, ldc)
+        paths.add(info(dev).path)
+        assert np.abs(got - want).max() <= 8e-16 * 2 * k * 2 + 1e-15, (m, n, k, ta, tb, lda, ldc)
+        if ldc > m:
+            pad_rows = np.arange(ldc * n).reshape(n, ldc)[:, m:].reshape(-1)
+            assert np.array_equal(got[pad_rows], c[pad_rows]), (m, n, k, ldc)
+    assert paths & {0, 1}
+
+
 def test_strided_equals_packed_and_ld_errors(dev):
     # tests/test_kernels.cpp:236-269
     rng = np.random.default_rng(31)
