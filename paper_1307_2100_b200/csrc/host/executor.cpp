@@ -729,8 +729,8 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
   }
   if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1, wait);
   if (stream_mode_ <= -2)
-    return run_streamed_f(left, right, out, slabs > 0 ? slabs : f_slabs_, -2 - stream_mode_,
-                          wait);
+    return run_streamed_f(left, right, out, slabs > 0 ? slabs : -f_slabs_, -2 - stream_mode_,
+                          wait);  // a negative count: chosen here, not by the caller
   // the stream label: outermost output label, outermost mode of its operand
   const auto& outs = v_.spec.output.indices;
   int label = outs.empty() ? -1 : v_.label_index(outs.back().label);
@@ -998,7 +998,8 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
   const LabelInfo& li = v_.labels[static_cast<std::size_t>(label)];
   const std::int64_t E = li.extent;
   const bool on_left = li.left_mode >= 0;
-  slabs = static_cast<int>(std::clamp<std::int64_t>(slabs, 1, E));
+  const bool auto_slabs = slabs < 0;
+  slabs = static_cast<int>(std::clamp<std::int64_t>(slabs < 0 ? -slabs : slabs, 1, E));
   int pinned_l = 0, pinned_r = 0, pinned_o = 0;
   tcb_host_is_pinned(left, &pinned_l);
   tcb_host_is_pinned(right, &pinned_r);
@@ -1015,9 +1016,41 @@ int PreparedContraction::run_streamed_f(const double* left, const double* right,
   const auto [bc, ac] = label_geom(v_, label, 2);
   std::map<std::int64_t, DeviceRecipe> recipes;  // one per distinct slab extent
   std::vector<std::int64_t> sizes;
-  for (int i = 0; i < slabs; ++i) {
-    const std::int64_t e = E / slabs + (i < E % slabs ? 1 : 0);
-    sizes.push_back(e);
+  for (int i = 0; i < slabs; ++i) sizes.push_back(E / slabs + (i < E % slabs ? 1 : 0));
+  // When the contraction, not the copies, bounds the call (cfg4: 61 ms of DMMA
+  // over 39 ms of PCIe each way), what stays outside the overlap is the first
+  // slab's upload and the last slab's download — a slab each (134 MB, 2.4 ms).
+  // A doubling ramp of small first slabs and its mirror at the end shrink both
+  // to a quarter (slab counts chosen here only; starting at an eighth measured 1 ms slower on cfg4: TC_SLAB_RAMP_DIV; rows of the 2-D copies stay
+  // >= 4 KB, which move at the full PCIe rate). TC_NO_SLAB_RAMP=1: equal slabs.
+  static const bool no_ramp = getenv("TC_NO_SLAB_RAMP") != nullptr;
+  if (auto_slabs && !no_ramp) {
+    const std::int64_t nominal = (E + slabs - 1) / slabs;
+    const double t_gpu = static_cast<double>(flop_count(v_)) / 3.4e13;
+    const double t_copy = static_cast<double>(std::max(on_left ? nl_ : nr_, no_)) * 8.0 / 5.5e10;
+    const std::int64_t min_e = std::max<std::int64_t>(
+        1, (4096 + 8 * std::min(bx, bc) - 1) / (8 * std::min(bx, bc)));
+    std::vector<std::int64_t> ramp;
+    static const std::int64_t ramp_div =
+        getenv("TC_SLAB_RAMP_DIV") ? std::max(2, atoi(getenv("TC_SLAB_RAMP_DIV"))) : 4;
+    for (std::int64_t e = std::max(min_e, nominal / ramp_div); e < nominal; e *= 2)
+      ramp.push_back(e);
+    std::int64_t ramp_sum = 0;
+    for (std::int64_t e : ramp) ramp_sum += e;
+    if (!ramp.empty() && t_gpu >= 0.8 * t_copy && E >= 2 * ramp_sum + 2 * nominal) {
+      sizes = ramp;
+      std::int64_t rest = E - 2 * ramp_sum;
+      while (rest > 0) {
+        std::int64_t e = std::min(rest, nominal);
+        if (rest - e > 0 && rest - e < (nominal + 1) / 2) e = rest;  // no sliver
+        sizes.push_back(e);
+        rest -= e;
+      }
+      for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) sizes.push_back(*it);
+      slabs = static_cast<int>(sizes.size());
+    }
+  }
+  for (const std::int64_t e : sizes) {
     if (recipes.count(e)) continue;
     ValidatedContraction sv = v_;
     sv.labels[static_cast<std::size_t>(label)].extent = e;
