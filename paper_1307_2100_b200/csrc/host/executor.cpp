@@ -750,6 +750,7 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
           !(ps.ext.back() == E && ps.src_str.back() * E == (on_left ? nl_ : nr_)))
         label = -1;
   }
+  const bool auto_slabs = slabs <= 0;
   if (label >= 0 && slabs <= 0) {
     // auto (decided once per prepared contraction): ~16 MB per slab in the
     // busier copy direction, up to 64 slabs, but no thinner than keeps both slab
@@ -812,22 +813,61 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     bool ok = groups_ok_;
     return lower_checked(sv, &ok);
   };
-  const std::int64_t base = E / slabs, extra = E % slabs;
-  DeviceRecipe rb = sub_recipe(base), rb1 = extra ? sub_recipe(base + 1) : rb;
-  // slab recipes must permute exactly the operands the full recipe does (its
-  // permutation buffers are the ones allocated)
+  // Slab extents: equal slabs; when the slab count was chosen here and the
+  // contraction outweighs the copies (a large plain matrix product), a
+  // doubling ramp of small first slabs and its mirror at the end, as in
+  // run_streamed_f (transfer-bound contractions gain nothing from it: cfg2,
+  // cfg3 measured, profiles/r02_experiments.jsonl).
+  std::vector<std::int64_t> sched;
+  for (int i = 0; i < slabs; ++i) sched.push_back(E / slabs + (i < E % slabs ? 1 : 0));
+  {
+    static const bool no_ramp = getenv("TC_NO_SLAB_RAMP") != nullptr;
+    static const std::int64_t ramp_div =
+        getenv("TC_SLAB_RAMP_DIV") ? std::max(2, atoi(getenv("TC_SLAB_RAMP_DIV"))) : 4;
+    const std::int64_t nominal = (E + slabs - 1) / slabs;
+    const double t_gpu = static_cast<double>(flop_count(v_)) / 3.4e13;
+    const double t_copy =
+        static_cast<double>(std::max(on_left ? nl_ : nr_, no_)) * 8.0 / 5.5e10;
+    std::vector<std::int64_t> ramp;
+    for (std::int64_t e = std::max<std::int64_t>(1, nominal / ramp_div); e < nominal; e *= 2)
+      ramp.push_back(e);
+    std::int64_t ramp_sum = 0;
+    for (std::int64_t e : ramp) ramp_sum += e;
+    if (auto_slabs && !no_ramp && !ramp.empty() && t_gpu >= 0.8 * t_copy &&
+        E >= 2 * ramp_sum + 2 * nominal) {
+      sched = ramp;
+      std::int64_t rest = E - 2 * ramp_sum;
+      while (rest > 0) {
+        std::int64_t e = std::min(rest, nominal);
+        if (rest - e > 0 && rest - e < (nominal + 1) / 2) e = rest;  // no sliver
+        sched.push_back(e);
+        rest -= e;
+      }
+      for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) sched.push_back(*it);
+    }
+  }
+  // slab recipes (one per distinct extent) must permute exactly the operands
+  // the full recipe does (its permutation buffers are the ones allocated)
   auto same_permutes = [&](const DeviceRecipe& x) {
     if (x.permutes.size() != recipe_.permutes.size()) return false;
     for (std::size_t i = 0; i < x.permutes.size(); ++i)
       if (x.permutes[i].right != recipe_.permutes[i].right) return false;
     return true;
   };
-  if (!same_permutes(rb) || !same_permutes(rb1)) {
+  std::map<std::int64_t, DeviceRecipe> slab_recipes;
+  bool recipes_ok = true;
+  for (std::int64_t e : sched)
+    if (!slab_recipes.count(e)) {
+      auto it = slab_recipes.emplace(e, sub_recipe(e)).first;
+      recipes_ok = recipes_ok && same_permutes(it->second);
+    }
+  if (!recipes_ok) {
     upload(left, right);
     run();
     download(out);
     return 1;
   }
+  slabs = static_cast<int>(sched.size());
 
   exec_mark("o-slabs: lowered");
   if (!pipes_) pipes_ = acquire_pipes(device_);
@@ -848,8 +888,8 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
   bool other_permuted = false;
   std::int64_t e0 = 0;
   for (int s = 0; s < slabs; ++s) {
-    const std::int64_t e = base + (s < extra ? 1 : 0);
-    const DeviceRecipe& r = (s < extra) ? rb1 : rb;
+    const std::int64_t e = sched[static_cast<std::size_t>(s)];
+    const DeviceRecipe& r = slab_recipes.at(e);
     check(tcb_memcpy_async(stream_dev + e0 * s_elems, stream_host + e0 * s_elems,
                            e * s_elems * 8, up),
           "upload");

@@ -1,5 +1,6 @@
 """Times the drop-in call (tcf_execute_host, pinned host buffers) on a BASELINE
-config: median of N calls after one warm-up. Usage: python tools/e2e_ab.py cfg5 [N]"""
+config, or on any expression: median of N calls after one warm-up.
+Usage: python tools/e2e_ab.py cfg5 [N]  |  python tools/e2e_ab.py "<expr>" "<extents>" [N]"""
 import ctypes as C
 import statistics
 import sys
@@ -11,8 +12,13 @@ import bench  # noqa: E402
 import paper_1307_2100_b200 as T  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-expr, ext, _ = bench.CONFIGS[cfg]
+if cfg in bench.CONFIGS:
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    expr, ext, _ = bench.CONFIGS[cfg]
+else:
+    expr, ext = sys.argv[1], sys.argv[2]
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    cfg = ext
 dev = T.native.device()
 T.check(dev.tcb_init(0))
 p = T.Prepared(expr, ext)
