@@ -725,7 +725,13 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
       }
     }
     const int kl = recipe_.permutes.empty() ? k_stream_label(v_) : -1;
-    if (kl >= 0 && no_ < other) stream_mode_ = 1 + kl;
+    // contracted-label slabs when the output is no larger than the operand the
+    // other modes upload whole (equal sizes — square matrix products — included:
+    // 12288^3 130.9 -> 122.1 ms, 16384^3 285.7 -> 278.5; with a larger output
+    // its download outlasts the last slab's contraction: 16384^2 x 8192 144 vs
+    // 160 ms, tools/gpu/run85.sh)
+    if (kl >= 0 && no_ <= other)
+      stream_mode_ = 1 + kl;
   }
   if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1, wait);
   if (stream_mode_ <= -2)
@@ -1209,6 +1215,22 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
       rest -= e;
       ramp = std::max(ramp + unit, ramp * 3 / 2);
     }
+    // The last slab's contraction hides the result's download (its column
+    // blocks go down as they finish, below) only if it lasts as long as that
+    // download: where the contraction outweighs the copies, trailing slabs
+    // merge until it does (8192^3: C takes 9.8 ms to download, an eighth of
+    // the contraction 4 ms; cfg5: 122 ms against 9.8, nothing to merge).
+    static const bool no_merge = getenv("TC_NO_LAST_MERGE") != nullptr;  // diagnostics
+    const double t_gpu = static_cast<double>(flop_count(v_)) / 3.4e13;
+    const double t_up = static_cast<double>(nl_ + nr_) * 8.0 / 5.5e10;
+    const double t_down = static_cast<double>(no_) * 8.0 / 5.5e10;
+    if (!no_merge && t_gpu >= 0.8 * t_up)
+      while (sizes.size() > 2 &&
+             t_gpu * static_cast<double>(sizes.back()) / static_cast<double>(E) < t_down &&
+             2 * (sizes.back() + sizes[sizes.size() - 2]) <= E) {
+        sizes[sizes.size() - 2] += sizes.back();
+        sizes.pop_back();
+      }
     slabs = static_cast<int>(sizes.size());
   }
   // The last slab's contraction is split into column blocks of the output's
