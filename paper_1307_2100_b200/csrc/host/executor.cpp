@@ -730,7 +730,15 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
     // 12288^3 130.9 -> 122.1 ms, 16384^3 285.7 -> 278.5; with a larger output
     // its download outlasts the last slab's contraction: 16384^2 x 8192 144 vs
     // 160 ms, tools/gpu/run85.sh)
-    if (kl >= 0 && no_ <= other)
+    // ... or, with a larger output, when the contraction is long enough that a
+    // merged last slab (at most half of the label, run_streamed_k) hides the
+    // result's download: download time <= 0.4 x contraction time
+    // (TC_STREAM_K_DOWN=<fraction>, diagnostics)
+    static const double k_down =
+        getenv("TC_STREAM_K_DOWN") ? atof(getenv("TC_STREAM_K_DOWN")) : 0.4;
+    const double t_gpu = static_cast<double>(flop_count(v_)) / 3.4e13;
+    const double t_down = static_cast<double>(no_) * 8.0 / 5.5e10;
+    if (kl >= 0 && (no_ <= other || t_down <= k_down * t_gpu))
       stream_mode_ = 1 + kl;
   }
   if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1, wait);
