@@ -1214,7 +1214,14 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     // contraction.
     const std::int64_t unit = ((sa | sb) & 1) ? 2 : 1;
     const std::int64_t nominal = std::max<std::int64_t>(unit, (E + 7) / 8 / unit * unit);
-    std::int64_t rest = E, ramp = unit;
+    // the ramp opens with a slab of at least 256 contracted elements (16
+    // k-blocks per tile): below that a slab GEMM is all epilogue (a plain
+    // 8192^3 product ramping from 2 spent 3 ms in ten slabs that rewrite the
+    // whole 537 MB of C for k = 2..94 each); cfg5's label unit is already 512
+    const std::int64_t per_unit = std::max<std::int64_t>(1, recipe_.k / E);
+    const std::int64_t open_e = std::min(
+        nominal, ((256 + per_unit - 1) / per_unit + unit - 1) / unit * unit);
+    std::int64_t rest = E, ramp = std::max(unit, open_e);
     while (rest > 0) {
       std::int64_t e = std::min({rest, ramp / unit * unit, nominal});
       e = std::max(e, std::min(rest, unit));
