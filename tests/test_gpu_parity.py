@@ -240,6 +240,57 @@ def test_streamed_host_path_matches(dev, name, e, x):
         dev.tcb_host_unregister(a.ctypes.data)
 
 
+@pytest.mark.parametrize("name,e,x,lsh,rsh,sub", [
+    # square product: contracted-label slabs, ramp from 256 contracted
+    # elements, trailing slabs merged so the last contraction hides C's download
+    ("k-merged-last", "C[+i,+j] = A[+i,+k] * B[-k,+j]", "i=6144,j=6144,k=6144",
+     (6144, 6144), (6144, 6144), "ik,kj->ij"),
+    # output larger than either operand, download > 0.4 x contraction: the
+    # output-label / free-label paths with ramped first and last slabs
+    ("o-ramp", "C[+i,+j] = A[+i,+k] * B[-k,+j]", "i=8192,j=8192,k=2048",
+     (8192, 2048), (2048, 8192), "ik,kj->ij"),
+    # cfg4's shape, smaller: free label b streams A and C, B goes up whole
+    ("f-ramp", "C[+a,+b,+i,+j] = A[+a,+b,+k,+l] * B[-k,-l,+i,+j]",
+     "a=128,b=128,i=48,j=48,k=48,l=48", (128, 128, 48, 48), (48, 48, 48, 48), "abkl,klij->abij"),
+])
+def test_streamed_auto_schedules_compute_bound(dev, name, e, x, lsh, rsh, sub):
+    """run_streamed with the slab schedule chosen by the engine (slabs = 0) on
+    contractions that outweigh their copies: ramped first / last slabs, the
+    merged last slab of the contracted-label path, the mode choice — against
+    numpy on sampled rows (relative Frobenius), and the same bits on a second
+    call (the schedule and the sums are deterministic)."""
+    p = T.Prepared(e, x)
+    inf = p.info()
+    rng = np.random.default_rng(len(name))
+    L = rng.uniform(-1, 1, inf["left"])
+    R = rng.uniform(-1, 1, inf["right"])
+    out = np.zeros(inf["output"])
+    for a in (L, R, out):
+        T.check(dev.tcb_host_register(a.ctypes.data, a.nbytes))
+    try:
+        used = p.run_streamed(L, R, out, slabs=0)
+        again = np.zeros_like(out)
+        T.check(dev.tcb_host_register(again.ctypes.data, again.nbytes))
+        try:
+            p.run_streamed(L, R, again, slabs=0)
+        finally:
+            dev.tcb_host_unregister(again.ctypes.data)
+    finally:
+        for a in (L, R, out):
+            dev.tcb_host_unregister(a.ctypes.data)
+    assert used >= 2, name
+    assert np.array_equal(out, again), name  # deterministic schedule and sums
+    # numpy on a sample of the leading index (Fortran-ordered operands)
+    Lf = L.reshape(lsh, order="F")
+    Rf = R.reshape(rsh, order="F")
+    osh = tuple(dict(zip(sub.split("->")[0].replace(",", ""), lsh + rsh))[c]
+                for c in sub.split("->")[1])
+    got = out.reshape(osh, order="F")
+    rows = rng.choice(lsh[0], size=24, replace=False)
+    want = np.einsum(sub, Lf[rows], Rf, optimize=True)
+    assert np.linalg.norm(got[rows] - want) <= TOL * np.linalg.norm(want), name
+
+
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4"])
 def test_full_size_scaling_is_exact_and_additive(dev, cfg):
     """Size-independent properties at the BASELINE sizes: scaling an operand
