@@ -324,7 +324,7 @@ std::int64_t slab_bytes() {
   return b;
 }
 
-int k_stream_label(const ValidatedContraction& v) {
+int k_stream_label(const ValidatedContraction& v, std::int64_t min_row = kMinRow) {
   int best = -1;
   std::int64_t best_rows = 0;
   for (int id : v.contracted) {
@@ -347,7 +347,7 @@ int k_stream_label(const ValidatedContraction& v) {
       }
       row_min = std::min(row_min, below * 8);
     }
-    if (!ok || row_min * li.extent < 2 * kMinRow) continue;
+    if (!ok || row_min * li.extent < 2 * min_row) continue;
     if (best < 0 || row_min > best_rows) {
       best = id;
       best_rows = row_min;
@@ -724,7 +724,15 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
         f_slabs_ = fs;
       }
     }
-    const int kl = recipe_.permutes.empty() ? k_stream_label(v_) : -1;
+    // (copy rows of 4 KB still move at the PCIe rate in large copies,
+    // tools/pcie.py; where the contraction outweighs the uploads that is
+    // enough — a plain product with K < 8192 has no 32 KB rows to offer;
+    // 6144^3: 19.8 -> 17.6 ms. At 0.8 x the uploads 4096^3 lost 13 %: 1.1 x)
+    const double t_gpu0 = static_cast<double>(flop_count(v_)) / 3.4e13;
+    const double t_up0 = static_cast<double>(nl_ + nr_) * 8.0 / 5.5e10;
+    static const bool narrow = getenv("TC_STREAM_K_NO_NARROW") == nullptr;  // diagnostics
+    const std::int64_t min_row = (narrow && t_gpu0 >= 1.1 * t_up0) ? (4 << 10) : kMinRow;
+    const int kl = recipe_.permutes.empty() ? k_stream_label(v_, min_row) : -1;
     // contracted-label slabs when the output is no larger than the operand the
     // other modes upload whole (equal sizes — square matrix products — included:
     // 12288^3 130.9 -> 122.1 ms, 16384^3 285.7 -> 278.5; with a larger output
@@ -738,7 +746,14 @@ int PreparedContraction::run_streamed(const double* left, const double* right, d
         getenv("TC_STREAM_K_DOWN") ? atof(getenv("TC_STREAM_K_DOWN")) : 0.4;
     const double t_gpu = static_cast<double>(flop_count(v_)) / 3.4e13;
     const double t_down = static_cast<double>(no_) * 8.0 / 5.5e10;
-    if (kl >= 0 && (no_ <= other || t_down <= k_down * t_gpu))
+    // (an output exactly as large as that operand — square products — only
+    // when the contraction outweighs the uploads: a transfer-bound square
+    // product would wait for C's download after the last slab;
+    // TC_STREAM_K_SQUARE=always|never overrides, diagnostics)
+    const double t_up = static_cast<double>(nl_ + nr_) * 8.0 / 5.5e10;
+    static const char* sq = getenv("TC_STREAM_K_SQUARE");
+    const bool square_ok = sq ? sq[0] == 'a' : t_gpu >= 1.1 * t_up;
+    if (kl >= 0 && (no_ < other || (no_ == other && square_ok) || t_down <= k_down * t_gpu))
       stream_mode_ = 1 + kl;
   }
   if (stream_mode_ > 0) return run_streamed_k(left, right, out, slabs, stream_mode_ - 1, wait);
@@ -1187,8 +1202,16 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
   };
   const auto [sa, ha] = geom(false);
   const auto [sb, hb] = geom(true);
-  // copy rows of at least 32 KB per slab
-  slabs = static_cast<int>(std::min<std::int64_t>(slabs, std::min(sa, sb) * 8 * E / kMinRow));
+  // copy rows of at least 32 KB per slab (4 KB when the engine chose the
+  // slabs for a contraction that outweighs its uploads, as in run_streamed)
+  {
+    const double t_gpu0 = static_cast<double>(flop_count(v_)) / 3.4e13;
+    const double t_up0 = static_cast<double>(nl_ + nr_) * 8.0 / 5.5e10;
+    static const bool narrow = getenv("TC_STREAM_K_NO_NARROW") == nullptr;
+    const std::int64_t min_row =
+        (auto_slabs && narrow && t_gpu0 >= 1.1 * t_up0) ? (4 << 10) : kMinRow;
+    slabs = static_cast<int>(std::min<std::int64_t>(slabs, std::min(sa, sb) * 8 * E / min_row));
+  }
   if (slabs < 2 || !(pinned_l && pinned_r && pinned_o)) {
     upload(left, right);
     run();
@@ -1219,8 +1242,10 @@ int PreparedContraction::run_streamed_k(const double* left, const double* right,
     // 8192^3 product ramping from 2 spent 3 ms in ten slabs that rewrite the
     // whole 537 MB of C for k = 2..94 each); cfg5's label unit is already 512
     const std::int64_t per_unit = std::max<std::int64_t>(1, recipe_.k / E);
+    const std::int64_t row_e = (4096 + 8 * std::min(sa, sb) - 1) / (8 * std::min(sa, sb));
     const std::int64_t open_e = std::min(
-        nominal, ((256 + per_unit - 1) / per_unit + unit - 1) / unit * unit);
+        nominal,
+        (std::max((256 + per_unit - 1) / per_unit, row_e) + unit - 1) / unit * unit);
     std::int64_t rest = E, ramp = std::max(unit, open_e);
     while (rest > 0) {
       std::int64_t e = std::min({rest, ramp / unit * unit, nominal});
